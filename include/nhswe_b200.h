@@ -1,0 +1,188 @@
+/*
+ * nhswe_b200.h -- C ABI of the B200-native adaptive non-hydrostatic SWE step.
+ *
+ * Drop-in boundary for the time-step hot path of the reference package
+ * `nhswe` (arXiv 2505.17025; /root/reference/pkg/src/nhswe).  Every entry
+ * point is a plain C function over device pointers and sizes (no torch
+ * types); all work is enqueued asynchronously on the caller's CUDA stream
+ * (`stream` is a cudaStream_t passed as void*, NULL = legacy stream).
+ * Functions return 0 on success or a negative NH_E* launch/argument code.
+ * Numerical failures (positivity, elliptic breakdown) are reported per
+ * member through nh_status records in device memory, which the caller reads
+ * after synchronising and maps to the reference exception types.
+ *
+ * State layout (reference grid.py:137-147 per field, plus a member axis):
+ *   h, hu, hw : float64 [B][N][2], C-contiguous, node j of element e at
+ *               index (b*N + e)*2 + j.
+ */
+#ifndef NHSWE_B200_H
+#define NHSWE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NH_ABI_VERSION 1
+
+/* bottom model kinds (reference bathymetry.py:66-184 + harness models) */
+#define NH_BOTTOM_FLAT 0          /* FlatBottom(h0)                         bathymetry.py:66-79   */
+#define NH_BOTTOM_PLATE 1         /* HammackPlate(h0, zeta0, b, alpha)      bathymetry.py:82-116  */
+#define NH_BOTTOM_QUARTIC_SLIDE 2 /* WhittakerSlide + SlideMotion           bathymetry.py:119-184 */
+#define NH_BOTTOM_SMOOTH_BOX 3    /* harness: tanh-edged box uplift (configs 2, 4)                */
+#define NH_BOTTOM_SLOPE_SLIDE 4   /* harness: Gaussian mound on a plane slope (configs 3, 5)      */
+
+/* boundary kinds (hydrostatic.py:29-52) */
+#define NH_BC_ABSORBING 0
+#define NH_BC_WALL 1
+
+/* step modes (adaptivity.py:127-163) */
+#define NH_MODE_HYDROSTATIC 0     /* predictor only                                   */
+#define NH_MODE_GLOBAL 1          /* predictor + correction on [0, N-1]                */
+#define NH_MODE_ADAPTIVE 2        /* predictor + criterion mask + correction on ranges */
+#define NH_MODE_CORRECT_GIVEN 3   /* no predictor: correct the input state on given flags
+                                     (corrector.apply_correction, corrector.py:485-498) */
+
+/* criterion kinds (adaptivity.py:21, 75-96) */
+#define NH_CRIT_ETA_OVER_D 0
+#define NH_CRIT_ETA_X 1
+#define NH_CRIT_U 2
+#define NH_CRIT_U_X 3
+#define NH_CRIT_W 4
+#define NH_CRIT_W_X 5
+
+/* status codes */
+#define NH_OK 0
+#define NH_ERR_POSITIVITY_ENTRY 1   /* rhs entry check: PositivityError(element, t) hydrostatic.py:101-103 */
+#define NH_ERR_POSITIVITY_STAGE1 2  /* _advance after stage 1: PositivityError(-1, t+dt) :216-217       */
+#define NH_ERR_POSITIVITY_STAGE2 3  /* _advance after stage 2: PositivityError(-1, t+dt)                */
+#define NH_ERR_SOLVE_NONFINITE 4    /* EllipticSolveError, corrector.py:356-357                        */
+#define NH_ERR_SOLVE_PIVOT 5        /* zero pivot in the condensed elimination (singular system)         */
+
+/* launch / argument errors (return values) */
+#define NH_E_ARG (-1)
+#define NH_E_CUDA (-2)
+#define NH_E_UNSUPPORTED (-3)
+
+/* Per-member grid, bottom and boundary description (312 bytes).
+ * Grid operator values must be the reference GridSpec's (grid.py:71-114):
+ * they are 1-4 ulp off closed forms and are copied, not recomputed. */
+typedef struct nh_member {
+    double x_left;          /* GridSpec.x_left                              */
+    double dx;              /* GridSpec.dx                                  */
+    double dt;              /* fixed step (driver.py:84)                    */
+    double eps;             /* sample-node inset 1e-9*dx (grid.py:87)       */
+    double two_over_dx;     /* 2.0/dx (grid.py:215)                         */
+    double weak_div[4];     /* M^-1 K, row-major                            */
+    double lift_left[2];
+    double lift_right[2];
+    double mass[4];
+    double stiffness[4];
+    double deriv_ref[4];
+    double bottom[12];      /* model parameters, see nh_pack_* in DESIGN.md */
+    int32_t bc_left;        /* NH_BC_*                                      */
+    int32_t bc_right;
+    int32_t bottom_kind;    /* NH_BOTTOM_*                                  */
+    int32_t reserved;
+} nh_member;
+
+/* Scheme constants shared by all members of one call. */
+typedef struct nh_scheme {
+    double g;               /* GRAVITY                                      */
+    double rho;             /* RHO_WATER                                    */
+    double k_nh;            /* Criterion.k_nh                               */
+    double c11, c12, c22;   /* FluxCoefficients (corrector.py:40-47)        */
+    int32_t mode;           /* NH_MODE_*                                    */
+    int32_t criterion;      /* NH_CRIT_*                                    */
+    int32_t enlarge;        /* Criterion.enlarge                            */
+    int32_t record_cfl;     /* track max advisory CFL (hydrostatic.py:199)  */
+} nh_scheme;
+
+/* Per-member result record, written by the device. */
+typedef struct nh_status {
+    uint64_t error_key;     /* all-ones = ok (caller initialises); else the smallest
+                               (step<<34)|(code<<30)|(element+1) seen        */
+    double cfl_max;         /* max advisory CFL seen (if record_cfl)        */
+    int64_t flagged;        /* flagged elements summed over the steps       */
+    int32_t steps_done;
+    int32_t any_hw;         /* any(hw != 0) of the output state (w/w_x fallback) */
+} nh_status;
+
+/* Optional outputs of nh_advance. */
+typedef struct nh_outputs {
+    uint32_t* flag_bits;    /* [n_steps][B][ceil(N/32)] per-step mask bits, or NULL */
+    double* p_nh;           /* [B][N][2] pressure of the last step (0 off ranges), or NULL */
+    const uint32_t* given_flags; /* NH_MODE_CORRECT_GIVEN: [B][ceil(N/32)] */
+} nh_outputs;
+
+int nh_abi_version(void);
+
+/* Advance B independent channels by n_steps fused time steps, in place.
+ * Replaces adaptivity.adaptive_step (adaptivity.py:127-163) called in the
+ * loop of driver.simulate (driver.py:81-87); with n_steps == 1 and mode
+ * NH_MODE_HYDROSTATIC it is hydrostatic.heun_step (hydrostatic.py:192-209),
+ * with NH_MODE_CORRECT_GIVEN it is corrector.apply_correction
+ * (corrector.py:485-498).  `time` [B] holds each member's t and is advanced
+ * by t += dt per step (hydrostatic.py:206-209).  `status` [B] is
+ * zero-initialised by the caller except error_key = ~0. */
+int nh_advance(const nh_member* members, int n_members, int n_elements,
+               double* h, double* hu, double* hw, double* time, int n_steps,
+               const nh_scheme* scheme, const nh_outputs* outputs,
+               nh_status* status, void* stream);
+
+/* Semi-discrete tendency, hydrostatic.rhs_operator (hydrostatic.py:88-184).
+ * Outputs t_h, t_hu, t_hw [B][N][2]. */
+int nh_rhs(const nh_member* members, int n_members, int n_elements,
+           const double* h, const double* hu, const double* hw, const double* time,
+           double g, double* t_h, double* t_hu, double* t_hw,
+           nh_status* status, void* stream);
+
+/* Nodal indicator values, adaptivity.criterion_values (adaptivity.py:75-96). */
+int nh_criterion(const nh_member* members, int n_members, int n_elements,
+                 const double* h, const double* hu, const double* hw, const double* time,
+                 int kind, double* values, void* stream);
+
+/* Elliptic coefficients on all elements, corrector.phi_term +
+ * assemble_coefficients (corrector.py:100-170).  coef [7][B][N][2] =
+ * s11, s12, s22, f1, f2, phi, d_x (s21 = -s11). */
+int nh_coefficients(const nh_member* members, int n_members, int n_elements,
+                    const double* h, const double* hu, const double* hw, const double* time,
+                    double g, double rho, double* coef, void* stream);
+
+/* LDG solve from given coefficients on flagged ranges, corrector._solve_batched
+ * / ldg_solve / solve_on_ranges (corrector.py:292-424).  coef as above
+ * (only s11, s12, s22, f1, f2 read), flags [B][ceil(N/32)] (ranges = maximal
+ * runs), outer_right [B][N] = outer hu trace used when element e ends a range
+ * (corrector.py:388-403).  Outputs p, hu [B][N][2] on flagged elements
+ * (untouched elsewhere). */
+int nh_ldg_solve(const nh_member* members, int n_members, int n_elements,
+                 const double* coef, const uint32_t* flags, const double* outer_right,
+                 double rho, double c11, double c12, double c22,
+                 double* p, double* hu, nh_status* status, void* stream);
+
+/* Vertical-momentum update from a solved pressure, corrector.correct_momentum
+ * (corrector.py:441-482): hw_out = hw_in + dt/rho * bottom pressure on flagged
+ * elements, hw_in elsewhere.  h = predictor depth, p [B][N][2] (0 off ranges),
+ * coef as produced by nh_coefficients (phi, d_x planes read). */
+int nh_correct_momentum(const nh_member* members, int n_members, int n_elements,
+                        const double* h, const double* p, const double* coef,
+                        const uint32_t* flags, double rho, const double* hw_in,
+                        double* hw_out, void* stream);
+
+/* Bottom channels at arbitrary points, BathymetryModel.sample
+ * (bathymetry.py:43-57): out [6][B][n_points] = d, d_x, d_t, d_tt, d_xt, d_xx. */
+int nh_bottom_sample(const nh_member* members, int n_members, const double* x, int n_points,
+                     const double* time, double* out, void* stream);
+
+/* Last CUDA runtime error string (diagnostics). */
+const char* nh_last_cuda_error(void);
+
+/* Launch geometry chosen for a member length (cluster size, tile, threads). */
+int nh_plan(int n_elements, int n_members, int* cluster, int* tile, int* threads,
+            int* smem_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NHSWE_B200_H */

@@ -1,0 +1,184 @@
+"""Device plumbing: parameter packing, uploads, status decoding.
+
+PyTorch is used only to own device memory and streams; every computation is
+one of the library's kernels (``_lib``).  Without a CUDA device every entry
+point raises -- there is deliberately no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError("no CUDA device: the B200 NH-SWE kernels have no CPU fallback")
+    return _lib.load()
+
+
+def stream_ptr():
+    return torch().cuda.current_stream().cuda_stream
+
+
+def dev(a, dtype=np.float64):
+    """Host array -> contiguous device tensor."""
+    t = torch()
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return t.from_numpy(arr).to("cuda", non_blocking=False)
+
+
+def ptr(x) -> int | None:
+    return None if x is None else x.data_ptr()
+
+
+# ------------------------------------------------------------------ packing
+
+BC_CODE = {"absorbing": _lib.BC_ABSORBING, "wall": _lib.BC_WALL}
+
+
+def member_record(grid, bathy, bcs, dt: float | None) -> np.ndarray:
+    """One nh_member record (include/nhswe_b200.h) for a (grid, bottom, bcs, dt)."""
+    if grid.poly_order != 1:
+        raise NotImplementedError("the B200 kernels implement the P1 discretisation only")
+    r = np.zeros(1, dtype=_lib.MEMBER_DTYPE)
+    r["x_left"] = grid.x_left
+    r["dx"] = grid.dx
+    r["dt"] = 0.0 if dt is None else dt
+    r["eps"] = 1e-9 * grid.dx
+    r["two_over_dx"] = 2.0 / grid.dx
+    r["weak_div"] = grid.weak_div.ravel()
+    r["lift_left"] = grid.lift_left
+    r["lift_right"] = grid.lift_right
+    r["mass"] = grid.mass.ravel()
+    r["stiffness"] = grid.stiffness.ravel()
+    r["deriv_ref"] = grid.deriv_ref.ravel()
+    kind, params = bathy.pack()
+    r["bottom_kind"] = kind
+    r["bottom"][0, :len(params)] = params
+    if bcs is not None:
+        r["bc_left"] = BC_CODE[bcs.left.kind]
+        r["bc_right"] = BC_CODE[bcs.right.kind]
+    return r
+
+
+def upload_members(records: np.ndarray):
+    """Structured member table -> device byte tensor."""
+    raw = np.ascontiguousarray(records).view(np.uint8)
+    return dev(raw, dtype=np.uint8)
+
+
+def new_status(n: int):
+    st = np.zeros(n, dtype=_lib.STATUS_DTYPE)
+    st["error_key"] = _lib.STATUS_OK_KEY
+    return dev(st.view(np.uint8), dtype=np.uint8)
+
+
+def read_status(t) -> np.ndarray:
+    return t.cpu().numpy().view(_lib.STATUS_DTYPE)
+
+
+def decode_error(key) -> tuple[int, int, int] | None:
+    key = int(key)
+    if key == 0xFFFFFFFFFFFFFFFF:
+        return None
+    return key >> 34, (key >> 30) & 15, (key & 0x3FFFFFFF) - 1
+
+
+def raise_for_status(status: np.ndarray, t0, dt, member: int = 0):
+    """Map a device error record to the reference exception types."""
+    from .corrector import EllipticSolveError
+    from .hydrostatic import PositivityError
+    err = decode_error(status["error_key"][member])
+    if err is None:
+        return
+    step, code, element = err
+    t = float(np.asarray(t0).ravel()[member]) if np.ndim(t0) else float(t0)
+    dtm = float(np.asarray(dt).ravel()[member]) if np.ndim(dt) else float(dt)
+    for _ in range(step):          # time accumulates as t + dt (hydrostatic.py:206)
+        t = t + dtm
+    if code == _lib.ERR_POSITIVITY_ENTRY:
+        raise PositivityError(element, t)
+    if code in (_lib.ERR_POSITIVITY_STAGE1, _lib.ERR_POSITIVITY_STAGE2):
+        raise PositivityError(-1, t + dtm)
+    if code == _lib.ERR_SOLVE_PIVOT:
+        raise EllipticSolveError(f"singular elliptic system (zero pivot in element {element})")
+    raise EllipticSolveError("non-finite elliptic solution")
+
+
+# ------------------------------------------------------------ small kernels
+
+def bottom_sample(model, x: np.ndarray, t: float):
+    lib = require_cuda()
+    rec = np.zeros(1, dtype=_lib.MEMBER_DTYPE)
+    kind, params = model.pack()
+    rec["bottom_kind"] = kind
+    rec["bottom"][0, :len(params)] = params
+    m = upload_members(rec)
+    xs = dev(np.ravel(x))
+    tt = dev(np.array([t], dtype=np.float64))
+    out = torch().empty((6, xs.numel()), dtype=torch().float64, device="cuda")
+    _lib.check(lib.nh_bottom_sample(ptr(m), 1, ptr(xs), xs.numel(), ptr(tt), ptr(out),
+                                    stream_ptr()), "nh_bottom_sample")
+    host = out.cpu().numpy()
+    shape = np.shape(x)
+    return tuple(host[i].reshape(shape) for i in range(6))
+
+
+def flags_to_bits(flags: np.ndarray) -> np.ndarray:
+    """bool [..., N] -> uint32 words [..., ceil(N/32)] (bit e%32 of word e//32)."""
+    f = np.asarray(flags, dtype=bool)
+    n = f.shape[-1]
+    nw = (n + 31) // 32
+    pad = np.zeros(f.shape[:-1] + (nw * 32,), dtype=bool)
+    pad[..., :n] = f
+    b = np.packbits(pad.reshape(f.shape[:-1] + (nw, 4, 8)), axis=-1, bitorder="little")
+    return np.ascontiguousarray(b.reshape(f.shape[:-1] + (nw, 4))).view(np.uint32)[..., 0]
+
+
+def bits_to_flags(bits: np.ndarray, n: int) -> np.ndarray:
+    b = np.ascontiguousarray(bits, dtype=np.uint32)
+    u8 = b.view(np.uint8)
+    f = np.unpackbits(u8.reshape(b.shape[:-1] + (-1,)), axis=-1, bitorder="little")
+    return f[..., :n].astype(bool)
+
+
+def scheme(mode: int, kind: str = "eta_over_d", k_nh: float = 1e-3, enlarge: bool = False,
+           flux=None, g: float = 9.81, rho: float = 1000.0, record_cfl: bool = True):
+    s = _lib.Scheme()
+    s.g = g
+    s.rho = rho
+    s.k_nh = k_nh
+    s.c11 = 0.5 if flux is None else flux.c11
+    s.c12 = -0.5 if flux is None else flux.c12
+    s.c22 = 0.0 if flux is None else flux.c22
+    s.mode = mode
+    s.criterion = _lib.CRIT[kind]
+    s.enlarge = 1 if enlarge else 0
+    s.record_cfl = 1 if record_cfl else 0
+    return s
+
+
+def advance(members, h, hu, hw, time, n_steps, sch, status, flag_bits=None, p_out=None,
+            given=None):
+    """Enqueue nh_advance on the current stream (device tensors in, in place)."""
+    lib = require_cuda()
+    B, N = h.shape[0], h.shape[1]
+    out = _lib.Outputs(ptr(flag_bits), ptr(p_out), ptr(given))
+    rc = lib.nh_advance(ptr(members), B, N, ptr(h), ptr(hu), ptr(hw), ptr(time), int(n_steps),
+                        ctypes.byref(sch), ctypes.byref(out), ptr(status), stream_ptr())
+    _lib.check(rc, "nh_advance")

@@ -1,0 +1,201 @@
+// extern "C" boundary (include/nhswe_b200.h): argument checks, launch
+// geometry, cluster launches.
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <mutex>
+#include "step_kernel.cuh"
+
+extern "C" {
+int nh_launch_rhs(const nh_member*, int, int, const double*, const double*, const double*,
+                  const double*, double, double*, double*, double*, nh_status*, cudaStream_t);
+int nh_launch_criterion(const nh_member*, int, int, const double*, const double*, const double*,
+                        const double*, int, double*, cudaStream_t);
+int nh_launch_coef(const nh_member*, int, int, const double*, const double*, const double*,
+                   const double*, double, double, double*, cudaStream_t);
+int nh_launch_bottom(const nh_member*, int, const double*, int, const double*, double*,
+                     cudaStream_t);
+int nh_launch_momentum(const nh_member*, int, int, const double*, const double*, const double*,
+                       const uint32_t*, double, const double*, double*, cudaStream_t);
+}
+
+namespace {
+
+constexpr int kE = 3;
+
+struct Plan {
+  int cluster, tile, threads;
+  size_t smem;
+};
+
+// Launch geometry for members of n elements.  Each CTA keeps `tile` own
+// elements plus NH_HALO on each side in shared memory; clusters are as small
+// as the 384-thread CTA allows for large ensembles (more members in flight),
+// and up to 8 CTAs for small ensembles (lower step latency).
+Plan make_plan(int n, int members) {
+  const int H = NH_HALO;
+  const int tile_max = kE * NH_STEP_MAX_THREADS - 2 * H;
+  int cmin = (n + tile_max - 1) / tile_max;
+  int c = cmin;
+  if ((long long)members * cmin < 148) {
+    int want = std::max(cmin, std::min(8, (int)((148 + members - 1) / members)));
+    // keep tiles >= 64 elements so halos stay small next to the tile
+    while (want > cmin && (n + want - 1) / want < 64) --want;
+    c = want;
+  }
+  Plan p;
+  p.cluster = c;
+  p.tile = (n + c - 1) / c;
+  int slots = p.tile + 2 * H;
+  int thr = (slots + kE - 1) / kE;
+  p.threads = std::max(32, ((thr + 31) / 32) * 32);
+  p.smem = nh_step_smem_bytes(p.threads, kE);
+  return p;
+}
+
+bool g_attr_done = false;
+std::mutex g_attr_mu;
+
+int set_attrs() {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (g_attr_done) return 0;
+  void* k = nh_step_kernel_ptr(kE);
+  size_t smax = nh_step_smem_bytes(NH_STEP_MAX_THREADS, kE);
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax) != cudaSuccess)
+    return NH_E_CUDA;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    return NH_E_CUDA;
+  void* ks = nh_solve_kernel_ptr(kE);
+  if (cudaFuncSetAttribute(ks, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    return NH_E_CUDA;
+  g_attr_done = true;
+  return 0;
+}
+
+int launch_cluster(void* kernel, void* args, int grid, int block, size_t smem, int cluster,
+                   cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(block, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* params[1] = {args};
+  cudaError_t e = cudaLaunchKernelExC(&cfg, kernel, params);
+  return e == cudaSuccess ? 0 : NH_E_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+int nh_abi_version(void) { return NH_ABI_VERSION; }
+
+int nh_plan(int n_elements, int n_members, int* cluster, int* tile, int* threads,
+            int* smem_bytes) {
+  if (n_elements < 2 || n_members < 1) return NH_E_ARG;
+  Plan p = make_plan(n_elements, n_members);
+  if (p.cluster > NH_MAX_CLUSTER) return NH_E_UNSUPPORTED;
+  if (cluster) *cluster = p.cluster;
+  if (tile) *tile = p.tile;
+  if (threads) *threads = p.threads;
+  if (smem_bytes) *smem_bytes = (int)p.smem;
+  return 0;
+}
+
+int nh_advance(const nh_member* members, int n_members, int n_elements, double* h, double* hu,
+               double* hw, double* time, int n_steps, const nh_scheme* scheme,
+               const nh_outputs* outputs, nh_status* status, void* stream) {
+  if (!members || !h || !hu || !hw || !time || !scheme || !status) return NH_E_ARG;
+  if (n_members < 1 || n_elements < 2 || n_steps < 0) return NH_E_ARG;
+  if (n_steps == 0) return 0;
+  const nh_scheme& sc = *scheme;
+  if (sc.mode < NH_MODE_HYDROSTATIC || sc.mode > NH_MODE_CORRECT_GIVEN) return NH_E_ARG;
+  if (sc.mode != NH_MODE_HYDROSTATIC && (sc.c12 != -0.5 || sc.c22 != 0.0))
+    return NH_E_UNSUPPORTED;   // condensed solve needs the alternating flux (physics.cuh)
+  if (sc.mode == NH_MODE_CORRECT_GIVEN && (!outputs || !outputs->given_flags)) return NH_E_ARG;
+  Plan p = make_plan(n_elements, n_members);
+  if (p.cluster > NH_MAX_CLUSTER) return NH_E_UNSUPPORTED;
+  int rc = set_attrs();
+  if (rc) return rc;
+  StepArgs a;
+  a.members = members;
+  a.h = h; a.hu = hu; a.hw = hw; a.time = time;
+  a.status = status;
+  a.flag_bits = outputs ? outputs->flag_bits : nullptr;
+  a.p_out = outputs ? outputs->p_nh : nullptr;
+  a.given = outputs ? outputs->given_flags : nullptr;
+  a.sch = sc;
+  a.B = n_members; a.N = n_elements; a.n_steps = n_steps;
+  a.cluster = p.cluster; a.tile = p.tile; a.nwords = (n_elements + 31) / 32;
+  return launch_cluster(nh_step_kernel_ptr(kE), &a, n_members * p.cluster, p.threads, p.smem,
+                        p.cluster, (cudaStream_t)stream);
+}
+
+int nh_rhs(const nh_member* members, int n_members, int n_elements, const double* h,
+           const double* hu, const double* hw, const double* time, double g, double* t_h,
+           double* t_hu, double* t_hw, nh_status* status, void* stream) {
+  if (!members || n_members < 1 || n_elements < 2) return NH_E_ARG;
+  return nh_launch_rhs(members, n_members, n_elements, h, hu, hw, time, g, t_h, t_hu, t_hw, status,
+                       (cudaStream_t)stream);
+}
+
+int nh_criterion(const nh_member* members, int n_members, int n_elements, const double* h,
+                 const double* hu, const double* hw, const double* time, int kind,
+                 double* values, void* stream) {
+  if (!members || n_members < 1 || n_elements < 2 || kind < 0 || kind > 5) return NH_E_ARG;
+  return nh_launch_criterion(members, n_members, n_elements, h, hu, hw, time, kind, values,
+                             (cudaStream_t)stream);
+}
+
+int nh_coefficients(const nh_member* members, int n_members, int n_elements, const double* h,
+                    const double* hu, const double* hw, const double* time, double g, double rho,
+                    double* coef, void* stream) {
+  if (!members || n_members < 1 || n_elements < 2) return NH_E_ARG;
+  return nh_launch_coef(members, n_members, n_elements, h, hu, hw, time, g, rho, coef,
+                        (cudaStream_t)stream);
+}
+
+int nh_ldg_solve(const nh_member* members, int n_members, int n_elements, const double* coef,
+                 const uint32_t* flags, const double* outer_right, double rho, double c11,
+                 double c12, double c22, double* p, double* hu, nh_status* status, void* stream) {
+  if (!members || n_members < 1 || n_elements < 2) return NH_E_ARG;
+  if (c12 != -0.5 || c22 != 0.0) return NH_E_UNSUPPORTED;
+  int rc = set_attrs();
+  if (rc) return rc;
+  const int tile_max = kE * NH_STEP_MAX_THREADS;
+  int c = (n_elements + tile_max - 1) / tile_max;
+  if (c > NH_MAX_CLUSTER) return NH_E_UNSUPPORTED;
+  int tile = (n_elements + c - 1) / c;
+  int thr = std::max(32, ((tile + kE - 1) / kE + 31) / 32 * 32);
+  SolveArgs a;
+  a.members = members; a.coef = coef; a.flags = flags; a.outer_right = outer_right;
+  a.p = p; a.hu = hu; a.status = status; a.rho = rho; a.c11 = c11;
+  a.B = n_members; a.N = n_elements; a.cluster = c; a.tile = tile;
+  a.nwords = (n_elements + 31) / 32;
+  return launch_cluster(nh_solve_kernel_ptr(kE), &a, n_members * c, thr, nh_solve_smem_bytes(thr),
+                        c, (cudaStream_t)stream);
+}
+
+int nh_correct_momentum(const nh_member* members, int n_members, int n_elements, const double* h,
+                        const double* p, const double* coef, const uint32_t* flags, double rho,
+                        const double* hw_in, double* hw_out, void* stream) {
+  if (!members || n_members < 1 || n_elements < 2) return NH_E_ARG;
+  return nh_launch_momentum(members, n_members, n_elements, h, p, coef, flags, rho, hw_in, hw_out,
+                            (cudaStream_t)stream);
+}
+
+int nh_bottom_sample(const nh_member* members, int n_members, const double* x, int n_points,
+                     const double* time, double* out, void* stream) {
+  if (!members || n_members < 1 || n_points < 0) return NH_E_ARG;
+  return nh_launch_bottom(members, n_members, x, n_points, time, out, (cudaStream_t)stream);
+}
+
+const char* nh_last_cuda_error(void) { return cudaGetErrorString(cudaGetLastError()); }
+
+}  // extern "C"

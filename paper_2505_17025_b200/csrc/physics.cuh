@@ -1,0 +1,238 @@
+// Element-level physics of one NH-SWE time step, in registers.
+//
+//  * face_flux / element_tendency : hydrostatic.py:88-184 (rhs_operator),
+//    hydrostatic-reconstruction Rusanov flux, volume + lift + g h d_x terms.
+//  * ldg_coefficients             : corrector.py:100-170 (phi_term,
+//    assemble_coefficients), general (sloped) formulas -- the reference's
+//    flat-bottom branches are bit-identical to them.
+//  * local_condense               : one element's 4x4 LDG block
+//    (corrector.py:173-234 sparsity, :329-349 values) eliminated to the
+//    "super-element" form
+//        a_e = ga + aa * a_{e-1} + ba * z_{e+1}
+//        z_e = gz + az * a_{e-1} + bz * z_{e+1}
+//    with a_e = P(node 1), z_e = Q(node 0) - c11 * P(node 0), P = p / rho,
+//    Q = hu.  With the reference's alternating flux (c12 = -1/2, c22 = 0)
+//    an element talks to its left neighbour only through a_{e-1} and to its
+//    right neighbour only through z_{e+1}, so the node-interleaved banded
+//    system that LAPACK dgbsv factorises (corrector.py:352) is solved exactly
+//    by a chain of these 2-scalar couplings.
+//  * merge                        : eliminating the shared unknowns of two
+//    adjacent super-elements gives a super-element of the same form; the
+//    parallel solve is a tree of merges (thread chunk -> warp -> CTA ->
+//    cluster) followed by the matching back-substitution.
+#pragma once
+#include "nh_common.cuh"
+
+struct Face {
+  double F1, F2L, F2R, F3;   // F2L = F2 + corr_left (used by the element left of the face)
+};
+
+// Interface state on one side: conserved values, u = hu/h, 1/h, depth.
+struct Side {
+  double h, hu, hw, u, rh, d;
+};
+
+NH_DEV Side make_side(double h, double hu, double hw, double d) {
+  Side s;
+  s.h = h; s.hu = hu; s.hw = hw; s.d = d;
+  s.rh = nh_rcp(h);
+  s.u = hu * s.rh;
+  return s;
+}
+
+NH_DEV Side ghost_side(const Side& in, int bc) {
+  Side s = in;
+  if (bc == NH_BC_WALL) { s.hu = -in.hu; s.u = -in.u; }
+  return s;
+}
+
+// hydrostatic.py:131-160 with the general (reconstructed) formulas.  They are
+// bit-identical to the plain branch when dL == dR: hLs == hL,
+// corr == 0, (hLs/hL) == 1.
+NH_DEV Face face_flux(const Side& L, const Side& R, double g, double& speed) {
+  const double hg = 0.5 * g;
+  double dm = fmin(L.d, R.d);
+  double hLs = fmax(L.h - (L.d - dm), 0.0);
+  double hRs = fmax(R.h - (R.d - dm), 0.0);
+  double cL = hg * (L.h * L.h - hLs * hLs);
+  double cR = hg * (R.h * R.h - hRs * hRs);
+  double aL = fabs(L.u) + sqrt(g * hLs);
+  double aR = fabs(R.u) + sqrt(g * hRs);
+  speed = fmax(aL, aR);
+  double lam = 0.5 * speed;
+  double qL = hLs * L.u, qR = hRs * R.u;
+  Face f;
+  f.F1 = 0.5 * (qL + qR) - lam * (hRs - hLs);
+  double F2 = 0.5 * (qL * L.u + qR * R.u + hg * (hLs * hLs + hRs * hRs)) - lam * (qR - qL);
+  double wL = (hLs == L.h) ? L.hw : (hLs * L.rh) * L.hw;
+  double wR = (hRs == R.h) ? R.hw : (hRs * R.rh) * R.hw;
+  f.F3 = 0.5 * (wL * L.u + wR * R.u) - lam * (wR - wL);
+  f.F2L = F2 + cL;
+  f.F2R = F2 + cR;
+  return f;
+}
+
+// Tendency of one element (hydrostatic.py:162-183).  n0/n1 = own nodes,
+// fl = face at its left, fr = face at its right, dx0/dx1 = bottom slope.
+NH_DEV void element_tendency(const nh_member& m, double g, const Side& n0, const Side& n1,
+                             const Face& fl, const Face& fr, double dx0, double dx1,
+                             double t[6]) {
+  const double hg = 0.5 * g;
+  double f20 = n0.hu * n0.u + (hg * n0.h) * n0.h;
+  double f21 = n1.hu * n1.u + (hg * n1.h) * n1.h;
+  double f30 = n0.u * n0.hw, f31 = n1.u * n1.hw;
+  const double* W = m.weak_div;
+  const double* lr = m.lift_right;
+  const double* ll = m.lift_left;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    double v1 = fma(n1.hu, W[2 * i + 1], n0.hu * W[2 * i]);
+    v1 = v1 - fr.F1 * lr[i];
+    t[0 + i] = v1 + fl.F1 * ll[i];
+    double v2 = fma(f21, W[2 * i + 1], f20 * W[2 * i]);
+    v2 = v2 - fr.F2L * lr[i];
+    v2 = v2 + fl.F2R * ll[i];
+    t[2 + i] = v2 + (g * (i ? n1.h : n0.h)) * (i ? dx1 : dx0);
+    double v3 = fma(f31, W[2 * i + 1], f30 * W[2 * i]);
+    v3 = v3 - fr.F3 * lr[i];
+    t[4 + i] = v3 + fl.F3 * ll[i];
+  }
+}
+
+// ---------------------------------------------------------------- LDG part
+
+struct Chan {     // bottom channels at one node
+  double d, d_x, d_t, d_tt, d_xt, d_xx;
+};
+
+struct NodeCoef {
+  double s11, s12, s22, f1, f2, phi;
+};
+
+// corrector.py:100-170 at one node; h_x / eta_x are the element derivatives.
+NH_DEV NodeCoef ldg_coefficients(double h, double hu, double hw, double h_x, double eta_x,
+                                 const Chan& b, double dt, double g, double rho) {
+  NodeCoef c;
+  double ih = nh_rcp(h);
+  double u = hu * ih;
+  double acc = -b.d_tt;
+  acc = acc + (-2.0 * u * b.d_xt - u * u * b.d_xx);
+  acc = acc + (g * b.d_x) * eta_x;
+  double quad = 4.0 + b.d_x * b.d_x;
+  c.phi = (rho * h / quad) * acc;
+  c.s22 = (3.0 * dt / rho) * ih;
+  c.s11 = (h_x - 1.5 * b.d_x) * ih;
+  c.s12 = (0.25 * rho / dt) * quad * ih;
+  c.f1 = (0.25 * quad * ih) * (c.phi * b.d_x + (rho / dt) * hu);
+  double f2 = (-2.0 * hw - (0.5 * b.d_x) * hu) * ih;
+  f2 = f2 - (0.5 * dt / rho) * quad * c.phi * ih;
+  c.f2 = f2 - 2.0 * b.d_t;
+  return c;
+}
+
+// Super-element coefficients (ga, aa, ba, gz, az, bz).
+struct Super {
+  double ga, aa, ba, gz, az, bz;
+};
+
+NH_DEV Super super_identity() { return Super{0.0, 1.0, 0.0, 0.0, 0.0, 1.0}; }
+
+// An element outside every range: a_e = 0 (next element starts a range with
+// P* = 0) and z_e = its uncorrected hu at node 0 (the outer trace seen by a
+// range ending just before it, corrector.py:398-399).
+NH_DEV Super super_gap(double hu0) { return Super{0.0, 0.0, 0.0, hu0, 0.0, 0.0}; }
+
+// Gauss-Jordan (no pivoting) on the 4x4 element block with three right-hand
+// sides [r | l | v]; l = (1, c11, 0, 0) carries a_{e-1}, v = (0, 0, 0, -1)
+// carries z_{e+1}.  Unknown order (P0, Q0, P1, Q1).  Returns false on a zero
+// or non-finite pivot.  rec = (u0, w0, v0, u3, w3, v3) for reconstruction.
+NH_DEV bool local_condense(const nh_member& m, const NodeCoef& c0, const NodeCoef& c1,
+                           double rho, double c11, bool range_end, Super& S, double rec[6]) {
+  const double* M = m.mass;
+  const double* K = m.stiffness;
+  double A[4][7];
+  const NodeCoef* cj[2] = {&c0, &c1};
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const NodeCoef& q = *cj[j];
+      double Mij = M[2 * i + j], Kij = K[2 * i + j];
+      A[2 * i][2 * j] = -Kij + Mij * q.s11;
+      A[2 * i][2 * j + 1] = Mij * (q.s12 / rho);
+      A[2 * i + 1][2 * j + 1] = -Kij + Mij * (-q.s11);
+      A[2 * i + 1][2 * j] = Mij * (rho * q.s22);
+    }
+    A[2 * i][4] = fma(M[2 * i + 1], c1.f1 / rho, M[2 * i] * (c0.f1 / rho));
+    A[2 * i + 1][4] = fma(M[2 * i + 1], c1.f2, M[2 * i] * c0.f2);
+  }
+  // faces (c12 = -1/2, c22 = 0): left  -Q* = -(Q0 + c11 (a - P0)),  -P* = -a
+  //                              right +P* = P1 (interior only), +Q* = z + c11 P1
+  A[1][1] -= 1.0;
+  A[1][0] += c11;
+  if (!range_end) A[2][2] += 1.0;
+  A[3][2] += c11;
+  A[0][5] = 1.0; A[1][5] = c11; A[2][5] = 0.0; A[3][5] = 0.0;
+  A[0][6] = 0.0; A[1][6] = 0.0; A[2][6] = 0.0; A[3][6] = -1.0;
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    double piv = A[k][k];
+    ok = ok && (piv != 0.0) && isfinite(piv);
+    double r = nh_rcp(piv);
+#pragma unroll
+    for (int c = k + 1; c < 7; ++c) A[k][c] *= r;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (i == k) continue;
+      double f = A[i][k];
+#pragma unroll
+      for (int c = k + 1; c < 7; ++c) A[i][c] = fma(-f, A[k][c], A[i][c]);
+    }
+  }
+  S.ga = A[2][4]; S.aa = A[2][5]; S.ba = A[2][6];
+  S.gz = fma(-c11, A[0][4], A[1][4]);
+  S.az = fma(-c11, A[0][5], A[1][5]);
+  S.bz = fma(-c11, A[0][6], A[1][6]);
+  rec[0] = A[0][4]; rec[1] = A[0][5]; rec[2] = A[0][6];
+  rec[3] = A[3][4]; rec[4] = A[3][5]; rec[5] = A[3][6];
+  return ok;
+}
+
+// Merge two adjacent super-elements L (left) and R (right).  Also returns the
+// back-substitution rows: A_L = AL . (1, a_in, z_in), Z_R = ZR . (1, a_in, z_in).
+NH_DEV Super merge(const Super& L, const Super& R, double AL[3], double ZR[3]) {
+  double iD = nh_rcp(1.0 - L.ba * R.az);
+  AL[0] = fma(L.ba, R.gz, L.ga) * iD;
+  AL[1] = L.aa * iD;
+  AL[2] = L.ba * R.bz * iD;
+  ZR[0] = fma(R.az, AL[0], R.gz);
+  ZR[1] = R.az * AL[1];
+  ZR[2] = fma(R.az, AL[2], R.bz);
+  Super o;
+  o.ga = fma(R.aa, AL[0], R.ga);
+  o.aa = R.aa * AL[1];
+  o.ba = fma(R.aa, AL[2], R.ba);
+  o.gz = fma(L.bz, ZR[0], L.gz);
+  o.az = fma(L.bz, ZR[1], L.az);
+  o.bz = L.bz * ZR[2];
+  return o;
+}
+
+NH_DEV Super merge2(const Super& L, const Super& R) {
+  double AL[3], ZR[3];
+  return merge(L, R, AL, ZR);
+}
+
+// Forward Riccati sweep state: the incoming a_{e-1} = s + t * z_e.
+// For one super-element with incoming (s, t): z_e = m + n z_{e+1}, and the
+// outgoing (s', t') for the next one.  Returns the elimination factors.
+NH_DEV void riccati_step(const Super& S, double& s, double& t, double& mm, double& nn) {
+  double rden = nh_rcp(1.0 - S.az * t);
+  mm = fma(S.az, s, S.gz) * rden;
+  nn = S.bz * rden;
+  double at = S.aa * t;
+  double s2 = fma(at, mm, fma(S.aa, s, S.ga));
+  double t2 = fma(at, nn, S.ba);
+  s = s2; t = t2;
+}

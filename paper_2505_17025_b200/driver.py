@@ -1,0 +1,187 @@
+"""Time loop entry points (reference driver.py:50-103) and the batched API.
+
+``simulate`` keeps the reference signature.  The whole fixed-dt loop is ONE
+launch of the fused step kernel: the member stays resident in shared memory
+across all steps and its state crosses HBM once in and once out.
+``loop_time`` is device time (CUDA events) of the stepping launches, the
+analogue of the reference's loop-only perf_counter.
+
+``Ensemble`` / ``simulate_ensemble`` are the batched extension (SURVEY.md
+§8(b)): B independent channels of equal N with per-member grids, dt, bottoms
+and boundary kinds, stepped together; members shard across GPUs with no
+communication on the step path (``paper_2505_17025_b200.parallel``).
+"""
+
+from __future__ import annotations
+
+import math
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as D
+from . import _lib
+from .adaptivity import Criterion, NonHydroMask, contiguous_ranges
+from .bathymetry import RHO_WATER
+from .corrector import FluxCoefficients
+from .grid import FlowState, NodalField
+from .scenarios import ScenarioSpec
+
+_MODES = {"hydrostatic": _lib.MODE_HYDROSTATIC, "global": _lib.MODE_GLOBAL,
+          "adaptive": _lib.MODE_ADAPTIVE}
+
+
+@dataclass
+class RunResult:
+    spec: ScenarioSpec
+    mode: str
+    criterion: Criterion | None
+    final_state: FlowState
+    final_p: NodalField | None
+    final_mask: NonHydroMask | None
+    gauge_times: np.ndarray
+    gauge_eta: np.ndarray
+    mask_history: list
+    mask_fraction_mean: float
+    loop_time: float
+
+    def config_echo(self) -> dict:
+        grid = self.spec.grid
+        c = self.criterion
+        return {"scenario": self.spec.name, "mode": self.mode,
+                "criterion": c.kind if c else None, "k_nh": c.k_nh if c else None,
+                "enlarge": c.enlarge if c else None, "dt": self.spec.dt,
+                "t_end": self.spec.t_end, "n_elements": grid.n_elements,
+                "poly_order": grid.poly_order, "x_left": grid.x_left,
+                "x_right": grid.x_right, "gauges": list(self.spec.gauges)}
+
+
+class Ensemble:
+    """Device-resident state of B channels with N elements each.
+
+    members: nh_member records (numpy MEMBER_DTYPE, length B); h, hu, hw:
+    CUDA float64 tensors (B, N, 2); time: CUDA float64 (B,).
+    """
+
+    def __init__(self, records: np.ndarray, h, hu, hw, time=None):
+        T = D.torch()
+        D.require_cuda()
+        self.records = np.ascontiguousarray(records)
+        self.members = D.upload_members(self.records)
+        self.B, self.N = int(h.shape[0]), int(h.shape[1])
+        self.h, self.hu, self.hw = h, hu, hw
+        self.time = time if time is not None else T.zeros(self.B, dtype=T.float64, device="cuda")
+        self.status = D.new_status(self.B)
+
+    @classmethod
+    def from_host(cls, records, h, hu, hw, time=None):
+        t = D.dev(np.zeros(len(records)) if time is None else np.asarray(time, dtype=np.float64))
+        return cls(records, D.dev(h), D.dev(hu), D.dev(hw), t)
+
+    def reset_status(self):
+        self.status = D.new_status(self.B)
+
+    def advance(self, n_steps: int, mode: str = "adaptive", criterion: Criterion | None = None,
+                flux: FluxCoefficients = FluxCoefficients(), g: float = 9.81,
+                rho: float = RHO_WATER, flag_bits=None, p_out=None):
+        """Enqueue n_steps fused steps on the current stream (asynchronous)."""
+        if mode not in _MODES:
+            raise ValueError(f"unknown mode {mode!r}")
+        if mode == "adaptive" and criterion is None:
+            raise ValueError("adaptive mode requires a criterion")
+        c = criterion if criterion is not None else Criterion("eta_over_d")
+        sch = D.scheme(_MODES[mode], c.kind, c.k_nh, c.enlarge, flux, g, rho)
+        D.advance(self.members, self.h, self.hu, self.hw, self.time, n_steps, sch, self.status,
+                  flag_bits, p_out)
+
+    def check(self, t0=None):
+        """Raise the reference exception for the first failed member, if any."""
+        st = D.read_status(self.status)
+        bad = np.flatnonzero(st["error_key"] != _lib.STATUS_OK_KEY)
+        if bad.size:
+            i = int(bad[0])
+            t0v = 0.0 if t0 is None else np.asarray(t0).ravel()[i]
+            D.raise_for_status(st, t0v, self.records["dt"][i], member=i)
+        return st
+
+
+def simulate(spec: ScenarioSpec, initial: FlowState, mode: str,
+             criterion: Criterion | None = None,
+             flux: FluxCoefficients = FluxCoefficients(), rho: float = RHO_WATER,
+             record_masks: bool = True) -> RunResult:
+    """Run the fixed-dt loop to completion (reference driver.py:50-103)."""
+    if mode not in _MODES:
+        raise ValueError(f"unknown mode {mode!r}")
+    if mode == "adaptive" and criterion is None:
+        raise ValueError("adaptive mode requires a criterion")
+    T = D.torch()
+    grid = spec.grid
+    n = grid.n_elements
+    n_steps = spec.n_steps
+    rec = D.member_record(grid, spec.bathymetry, spec.bcs, spec.dt)
+    ens = Ensemble.from_host(rec, initial.h.values[None], initial.hu.values[None],
+                             initial.hw.values[None], [initial.time])
+    nw = (n + 31) // 32
+    record = record_masks and mode == "adaptive"
+    gauge_idx = [grid.nearest_node(x) for x in spec.gauges]
+    per_step = len(gauge_idx) > 0
+    bits = None
+    if mode != "hydrostatic":
+        bits = T.zeros((max(n_steps, 1), 1, nw), dtype=T.int32, device="cuda")
+    p = T.zeros_like(ens.h) if mode != "hydrostatic" else None
+    gauge_h = np.empty((n_steps + 1, len(gauge_idx)))
+    times = np.empty(n_steps + 1)
+    times[0] = initial.time
+    if per_step:
+        gauge_h[0] = [initial.h.values[e, j] for e, j in gauge_idx]
+    ev0, ev1 = T.cuda.Event(enable_timing=True), T.cuda.Event(enable_timing=True)
+    loop_ms = 0.0
+    if n_steps > 0:
+        if not per_step:
+            ev0.record()
+            ens.advance(n_steps, mode, criterion, flux, spec.g, rho, bits, p)
+            ev1.record()
+            ev1.synchronize()
+            loop_ms = ev0.elapsed_time(ev1)
+        else:
+            ge = T.as_tensor([e for e, _ in gauge_idx], device="cuda")
+            gj = T.as_tensor([j for _, j in gauge_idx], device="cuda")
+            for s in range(n_steps):
+                ev0.record()
+                ens.advance(1, mode, criterion, flux, spec.g, rho,
+                            bits[s:s + 1] if bits is not None else None, p)
+                ev1.record()
+                ev1.synchronize()
+                loop_ms += ev0.elapsed_time(ev1)
+                gauge_h[s + 1] = ens.h[0, ge, gj].cpu().numpy()
+    st = ens.check([initial.time])
+    t = initial.time
+    for s in range(n_steps):
+        t = t + spec.dt
+        times[s + 1] = t
+    final = FlowState._wrap(NodalField._wrap(grid, ens.h[0].cpu().numpy()),
+                            NodalField._wrap(grid, ens.hu[0].cpu().numpy()),
+                            NodalField._wrap(grid, ens.hw[0].cpu().numpy()), float(ens.time.item()))
+    if st["cfl_max"][0] > 1.0:
+        warnings.warn(f"advisory CFL number {st['cfl_max'][0]:.3f} exceeded 1 during the run",
+                      RuntimeWarning, stacklevel=2)
+    mask_history, final_mask, final_p = [], None, None
+    if mode == "hydrostatic":
+        final_mask = NonHydroMask.from_flags(np.zeros(n, dtype=bool)) if n_steps else None
+    elif n_steps:
+        allbits = bits.cpu().numpy().view(np.uint32)[:, 0]
+        last = D.bits_to_flags(allbits[-1], n)
+        final_mask = NonHydroMask.from_flags(last)
+        final_p = NodalField._wrap(grid, p[0].cpu().numpy()) if last.any() else None
+        if record:
+            flags = D.bits_to_flags(allbits, n)
+            mask_history = [(s, times[s + 1], contiguous_ranges(flags[s])) for s in range(n_steps)]
+    gauge_eta = np.empty((n_steps + 1, len(gauge_idx)))
+    if per_step:
+        gx = np.array([grid.sample_nodes[e, j] for e, j in gauge_idx])
+        for r in range(n_steps + 1):
+            gauge_eta[r] = gauge_h[r] - spec.bathymetry.depth(gx, times[r])
+    frac = float(st["flagged"][0]) / (n_steps * n) if (n_steps and mode != "hydrostatic") else 0.0
+    return RunResult(spec, mode, criterion, final, final_p, final_mask, times, gauge_eta,
+                     mask_history, frac, loop_ms * 1e-3)
