@@ -1,0 +1,101 @@
+"""GPU multi-step parity: simulate (one fused launch for the whole loop) and the
+batched ensemble path, against the oracle run step by step."""
+
+import numpy as np
+import pytest
+
+import paper_2505_17025_b200 as P
+from paper_2505_17025_b200 import configs
+from oracle import nhswe_oracle as O
+from tests.helpers import oracle_depth, oracle_member, rel
+
+pytestmark = pytest.mark.gpu
+
+
+def oracle_history(mem, h, hu, hw, n_steps, mode, kind="eta_over_d", k_nh=1e-3, enlarge=False):
+    """Oracle run keeping per-step flags and criterion values."""
+    t = 0.0
+    flags, vals = [], []
+    for _ in range(n_steps):
+        ph, pq, pw = O.heun(mem.grid, mem.bottom, mem.bcs, mem.g, h, hu, hw, t, mem.dt,
+                            cfl_warn=False)
+        o = O.step(mem, h, hu, hw, t, mode, kind, k_nh, enlarge, cfl_warn=False)
+        t = t + mem.dt
+        vals.append(O.indicator(mem.grid, mem.bottom, kind, ph, pq, pw, t).max(axis=1))
+        flags.append(o.flags)
+        h, hu, hw = o.h, o.hu, o.hw
+    return h, hu, hw, np.array(flags), np.array(vals)
+
+
+@pytest.mark.parametrize("mode", ["global", "adaptive"])
+def test_config1_simulate_prefix(mode):
+    cfg = configs.config1()
+    m = cfg.member(0)
+    h, hu, hw = cfg.host_state(0, None)
+    n_steps = 300
+    spec = P.ScenarioSpec("c1", m.grid, m.dt, n_steps * m.dt, m.bathymetry, m.bcs)
+    assert spec.n_steps == n_steps
+    init = P.FlowState(P.NodalField(m.grid, h), P.NodalField(m.grid, hu),
+                       P.NodalField(m.grid, hw), 0.0)
+    crit = P.Criterion("eta_over_d") if mode == "adaptive" else None
+    res = P.simulate(spec, init, mode, crit)
+    mem = oracle_member(m.grid, m.bathymetry, m.bcs, m.dt)
+    oh, oq, ow, oflags, ovals = oracle_history(mem, h, hu, hw, n_steps, mode)
+    assert rel(res.final_state.h.values - 1.0, oh - 1.0) <= 1e-9
+    assert rel(res.final_state.hu.values, oq) <= 1e-9
+    if mode == "adaptive":
+        assert len(res.mask_history) == n_steps
+        for s, (_, _, ranges) in enumerate(res.mask_history):
+            g = np.zeros(m.grid.n_elements, bool)
+            for e0, e1 in ranges:
+                g[e0:e1 + 1] = True
+            diff = np.flatnonzero(g != oflags[s])
+            near = np.abs(ovals[s][diff] - 1e-3) <= 1e-9 * 1e-3
+            assert near.all(), f"step {s}: mask differs at {diff[~near][:8]}"
+        assert abs(res.mask_fraction_mean - oflags.mean()) < 1e-3
+
+
+def test_long_member_cluster_global():
+    """N = 16384: one member spread over a 15-CTA cluster (DSMEM tree)."""
+    grid = P.GridSpec(0.0, 20.0, 16384)
+    bathy = P.SlopeGaussianSlide(0.1, np.tan(np.radians(12.0)), 1.0, 0.1, 0.4, 2.0, 1.5, 0.5, 0.8)
+    bcs = P.BoundaryPair(P.WALL, P.ABSORBING)
+    d = oracle_depth(bathy, grid.sample_nodes, 0.0)
+    x = grid.nodes
+    h = d + 0.01 * np.exp(-((x - 6.0) / 0.5) ** 2)
+    hu = 0.02 * np.exp(-((x - 6.0) / 0.5) ** 2)
+    hw = np.zeros_like(h)
+    dt = 6.5e-5
+    st = P.FlowState(P.NodalField(grid, h), P.NodalField(grid, hu), P.NodalField(grid, hw), 0.0)
+    mem = oracle_member(grid, bathy, bcs, dt)
+    t = 0.0
+    oh, oq, ow = h, hu, hw
+    for _ in range(6):
+        st = P.adaptive_step(st, dt, bathy, bcs, mode="global", cfl_warn=False).state
+        o = O.step(mem, oh, oq, ow, t, "global", cfl_warn=False)
+        oh, oq, ow = o.h, o.hu, o.hw
+        t += dt
+    assert rel(st.hu.values, oq) <= 1e-10
+    assert np.abs(st.hw.values - ow).max() <= 1e-10 * np.abs(ow).max()
+
+
+def test_ensemble_mixed_members():
+    """Config-4 style mixed ensemble (solitary + box uplift), per-member dt / dx."""
+    cfg = configs.Config4(n_members=6, n_elements=512, n_steps=120)
+    recs = cfg.records()
+    states = [cfg.host_state(i, oracle_depth) for i in range(cfg.n_members)]
+    H = np.stack([s[0] for s in states])
+    Q = np.stack([s[1] for s in states])
+    Wv = np.stack([s[2] for s in states])
+    ens = P.Ensemble.from_host(recs, H, Q, Wv)
+    crit = P.Criterion("eta_over_d")
+    ens.advance(cfg.n_steps, "adaptive", crit)
+    st = ens.check()
+    gh, gq, gw = (x.cpu().numpy() for x in (ens.h, ens.hu, ens.hw))
+    for i in range(cfg.n_members):
+        m = cfg.member(i)
+        mem = oracle_member(m.grid, m.bathymetry, m.bcs, m.dt)
+        r = O.run(mem, H[i], Q[i], Wv[i], cfg.n_steps, mode="adaptive")
+        assert rel(gh[i] - m.bathymetry.h0, r.h - m.bathymetry.h0) <= 1e-9, i
+        assert rel(gq[i], r.hu) <= 1e-9, i
+        assert abs(st["flagged"][i] / (cfg.n_steps * cfg.n_elements) - r.fraction_mean) < 1e-3
