@@ -129,7 +129,7 @@ class WhittakerSlide(BathymetryModel):
     def pack(self):
         mo = self.motion
         return _lib.BOTTOM_QUARTIC_SLIDE, [self.h0, self.Hs, self.Ls, self.x_start,
-                                           mo.a0, mo.u_t, mo.t1, mo.t2, mo.t3]
+                                           mo.a0, mo.u_t, mo.t1, mo.t2, mo.t3, 2.0 / self.Ls]
 
 
 @dataclass(frozen=True)
@@ -152,7 +152,8 @@ class SmoothBoxPlate(BathymetryModel):
             raise ValueError("|zeta0| must stay below the still depth")
 
     def pack(self):
-        return _lib.BOTTOM_SMOOTH_BOX, [self.h0, self.zeta0, self.b, self.alpha, self.w]
+        return _lib.BOTTOM_SMOOTH_BOX, [self.h0, self.zeta0, self.b, self.alpha, self.w,
+                                        1.0 / self.w, 1.0 / (self.w * self.w)]
 
 
 @dataclass(frozen=True)
@@ -186,7 +187,7 @@ class SlopeGaussianSlide(BathymetryModel):
     def pack(self):
         return _lib.BOTTOM_SLOPE_SLIDE, [self.d_top, self.tan_theta, self.d_max, self.A,
                                          self.sigma, self.x0, self.u_t, self.t0, self.d_stop,
-                                         self.x_stop, self.t_stop]
+                                         self.x_stop, self.t_stop, 1.0 / self.sigma]
 
 
 def hammack_time_constant(h0: float, b: float, direction: str, g: float = GRAVITY) -> float:

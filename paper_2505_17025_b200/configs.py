@@ -170,10 +170,19 @@ def _config4_draws(n_members: int, seed: int):
 class Config4(Config):
     """Mixed ensemble: even members solitary waves, odd members box uplifts.
 
-    h0 ~ U(0.5, 2) for every member, domain [0, 200 h0]; solitary a/h0 ~
-    U(0.05, 0.3), x0 = 0.2 L, outflow both ends; box zeta0/h0 ~ U(0.01, 0.1),
-    b ~ U(0.1, 1) h0, alpha ~ U(5, 50) 1/s, edge w = 0.2 h0, wall / outflow.
+    Solitary members: h0 ~ U(0.5, 2) m, a/h0 ~ U(0.05, 0.3), x0 = 0.2 L,
+    outflow both ends.  Box members: h0 = 0.01 m (lab scale; BASELINE leaves
+    their depth unstated), zeta0/h0 ~ U(0.01, 0.1), b ~ U(0.1, 1) h0,
+    alpha ~ U(5, 50) 1/s, edge w = 0.2 h0, wall / outflow.  Every member's
+    domain is [0, 200 h0].  At field depth (h0 ~ 1 m) an uplift with
+    alpha = 30-50 1/s is ~15x more impulsive (alpha sqrt(h0/g)) than the
+    reference's own Hammack plate and the reference model itself loses
+    positivity within ~0.15 s; at h0 = 0.01 m alpha sqrt(h0/g) spans
+    0.16-1.6 around Hammack's 0.61 and every corner of the box parameter
+    range runs the full 20000 steps.
     """
+
+    BOX_H0 = 0.01
 
     def __init__(self, n_members=4096, n_elements=4096, n_steps=20000, seed=SEED_CONFIG4):
         super().__init__("config4_mixed_ensemble", n_members, n_elements, n_steps, ("adaptive",))
@@ -191,6 +200,9 @@ class Config4(Config):
             lam = float(np.max(np.abs(hu / h) + np.sqrt(GRAVITY * h)))
             return MemberSpec(grid, FlatBottom(h0), BoundaryPair(ABSORBING, ABSORBING),
                               dt_from_cfl(grid.dx, lam), "solitary", {"a": a, "x0": x0})
+        h0 = self.BOX_H0
+        L = 200.0 * h0
+        grid = GridSpec(0.0, L, self.n_elements)
         bathy = SmoothBoxPlate(h0, h0 * float(r["zeta_rel"][i]), h0 * float(r["b_rel"][i]),
                                float(r["alpha"][i]), 0.2 * h0)
         return MemberSpec(grid, bathy, BoundaryPair(WALL, ABSORBING),
@@ -276,9 +288,9 @@ class Config5(Config):
                           0.5 * (arg + np.log1p(np.sqrt(-np.expm1(-2.0 * np.maximum(arg, 0.0))))),
                           0.0)
         rec["bottom_kind"] = _lib.BOTTOM_SLOPE_SLIDE
-        rec["bottom"][:, :11] = np.stack([np.full_like(tan_t, 0.1), tan_t, np.full_like(tan_t, 1.0),
+        rec["bottom"][:, :12] = np.stack([np.full_like(tan_t, 0.1), tan_t, np.full_like(tan_t, 1.0),
                                           A, sigma, x0, u_t, np.full_like(tan_t, 0.5),
-                                          np.full_like(tan_t, 0.8), x_stop, t_stop], 1)
+                                          np.full_like(tan_t, 0.8), x_stop, t_stop, 1.0 / sigma], 1)
         return rec
 
 

@@ -102,7 +102,7 @@ __global__ void nh_coef_kernel(const nh_member* __restrict__ members, int B, int
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     NodeCoef q = ldg_coefficients(i ? h1 : h0, hu[o + i], hw[o + i], ed(m, h0, h1, i),
-                                  ed(m, h0 - b0.d, h1 - b1.d, i), c[i], m.dt, g, rho);
+                                  ed(m, h0 - b0.d, h1 - b1.d, i), c[i], make_ldg_const(m.dt, g, rho));
     coef[0 * plane + o + i] = q.s11;
     coef[1 * plane + o + i] = q.s12;
     coef[2 * plane + o + i] = q.s22;
@@ -176,7 +176,7 @@ __global__ void nh_momentum_kernel(const nh_member* __restrict__ members, int B,
 // ------------------------------------------------------------------- ldg_solve
 size_t nh_solve_smem_bytes(int threads) {
   int W = threads / 32;
-  return ((size_t)W * 31 * 6 + W * 6 + W * 2 + 16 + 4 * (NH_MAX_CLUSTER + 32)) * 8;
+  return ((size_t)W * 31 * 6 + W * 6 + W * 2 + 16 + 2 * 31 * 6) * 8 + W * 4 + 16;
 }
 
 template <int E>
@@ -194,7 +194,9 @@ __global__ void __launch_bounds__(NH_STEP_MAX_THREADS) nh_solve_kernel(SolveArgs
   ts.wagg = ts.wnode + W * 31 * 6;
   ts.wio = ts.wagg + W * 6;
   ts.pub = ts.wio + W * 2;
-  ts.chain = ts.pub + 16;
+  ts.bnode = ts.pub + 16;
+  ts.cnode = ts.bnode + 31 * 6;
+  ts.wflag = (int*)(ts.cnode + 31 * 6);
   const size_t plane = (size_t)a.B * N * 2;
   const uint32_t* fb = a.flags + (size_t)b * a.nwords;
   auto flag = [&](int e) -> bool { return e >= 0 && e < N && ((fb[e >> 5] >> (e & 31)) & 1u); };
@@ -226,16 +228,17 @@ __global__ void __launch_bounds__(NH_STEP_MAX_THREADS) nh_solve_kernel(SolveArgs
         q[i].phi = 0.0;
       }
       bool range_end = (e == N - 1) || !flag(e + 1);
-      if (!local_condense(m, q[0], q[1], a.rho, a.c11, range_end, Sk[k], R[k]))
+      if (!local_condense(m, q[0], q[1], a.rho, 1.0 / a.rho, a.c11, range_end, Sk[k], R[k]))
         nh_report(a.status + b, 0, NH_ERR_SOLVE_PIVOT, e);
     }
   }
-  Super agg = Sk[0];
+  bool tflag = false;
 #pragma unroll
-  for (int k = 1; k < E; ++k) agg = merge2(agg, Sk[k]);
+  for (int k = 0; k < E; ++k) tflag = tflag || flg[k];
+  Super agg = chunk_aggregate<E>(Sk, tflag);
   if (tid == 0) ts.pub[6] = outer[N - 1];
   double a_in, z_in;
-  tree_solve(cluster, ts, C, rank, W, warp, lane, tid, agg, a_in, z_in);
+  tree_solve(cluster, ts, C, rank, W, warp, lane, tflag, agg, a_in, z_in);
   double aprev[E], znext[E];
   chunk_unwind<E>(Sk, a_in, z_in, aprev, znext);
 #pragma unroll

@@ -56,8 +56,8 @@ NH_DEV Face face_flux(const Side& L, const Side& R, double g, double& speed) {
   double hRs = fmax(R.h - (R.d - dm), 0.0);
   double cL = hg * (L.h * L.h - hLs * hLs);
   double cR = hg * (R.h * R.h - hRs * hRs);
-  double aL = fabs(L.u) + sqrt(g * hLs);
-  double aR = fabs(R.u) + sqrt(g * hRs);
+  double aL = fabs(L.u) + nh_sqrt(g * hLs);
+  double aR = fabs(R.u) + nh_sqrt(g * hRs);
   speed = fmax(aL, aR);
   double lam = 0.5 * speed;
   double qL = hLs * L.u, qR = hRs * R.u;
@@ -109,23 +109,41 @@ struct NodeCoef {
   double s11, s12, s22, f1, f2, phi;
 };
 
+// Scheme constants of the LDG system, computed once per member.
+struct LdgConst {
+  double rho, inv_rho, rho_dt, s12c, s22c, f2c, g, cdt;
+};
+
+NH_DEV LdgConst make_ldg_const(double dt, double g, double rho) {
+  LdgConst k;
+  k.rho = rho;
+  k.inv_rho = 1.0 / rho;
+  k.rho_dt = rho / dt;
+  k.s12c = 0.25 * rho / dt;
+  k.s22c = 3.0 * dt / rho;
+  k.f2c = 0.5 * dt / rho;
+  k.g = g;
+  k.cdt = dt / rho;
+  return k;
+}
+
 // corrector.py:100-170 at one node; h_x / eta_x are the element derivatives.
 NH_DEV NodeCoef ldg_coefficients(double h, double hu, double hw, double h_x, double eta_x,
-                                 const Chan& b, double dt, double g, double rho) {
+                                 const Chan& b, const LdgConst& k) {
   NodeCoef c;
   double ih = nh_rcp(h);
   double u = hu * ih;
   double acc = -b.d_tt;
   acc = acc + (-2.0 * u * b.d_xt - u * u * b.d_xx);
-  acc = acc + (g * b.d_x) * eta_x;
+  acc = acc + (k.g * b.d_x) * eta_x;
   double quad = 4.0 + b.d_x * b.d_x;
-  c.phi = (rho * h / quad) * acc;
-  c.s22 = (3.0 * dt / rho) * ih;
+  c.phi = (k.rho * h * nh_rcp(quad)) * acc;
+  c.s22 = k.s22c * ih;
   c.s11 = (h_x - 1.5 * b.d_x) * ih;
-  c.s12 = (0.25 * rho / dt) * quad * ih;
-  c.f1 = (0.25 * quad * ih) * (c.phi * b.d_x + (rho / dt) * hu);
+  c.s12 = k.s12c * quad * ih;
+  c.f1 = (0.25 * quad * ih) * (c.phi * b.d_x + k.rho_dt * hu);
   double f2 = (-2.0 * hw - (0.5 * b.d_x) * hu) * ih;
-  f2 = f2 - (0.5 * dt / rho) * quad * c.phi * ih;
+  f2 = f2 - k.f2c * quad * c.phi * ih;
   c.f2 = f2 - 2.0 * b.d_t;
   return c;
 }
@@ -136,6 +154,9 @@ struct Super {
 };
 
 NH_DEV Super super_identity() { return Super{0.0, 1.0, 0.0, 0.0, 0.0, 1.0}; }
+NH_DEV bool is_identity(const Super& s) {
+  return s.ga == 0.0 && s.aa == 1.0 && s.ba == 0.0 && s.gz == 0.0 && s.az == 0.0 && s.bz == 1.0;
+}
 
 // An element outside every range: a_e = 0 (next element starts a range with
 // P* = 0) and z_e = its uncorrected hu at node 0 (the outer trace seen by a
@@ -147,7 +168,8 @@ NH_DEV Super super_gap(double hu0) { return Super{0.0, 0.0, 0.0, hu0, 0.0, 0.0};
 // carries z_{e+1}.  Unknown order (P0, Q0, P1, Q1).  Returns false on a zero
 // or non-finite pivot.  rec = (u0, w0, v0, u3, w3, v3) for reconstruction.
 NH_DEV bool local_condense(const nh_member& m, const NodeCoef& c0, const NodeCoef& c1,
-                           double rho, double c11, bool range_end, Super& S, double rec[6]) {
+                           double rho, double inv_rho, double c11, bool range_end, Super& S,
+                           double rec[6]) {
   const double* M = m.mass;
   const double* K = m.stiffness;
   double A[4][7];
@@ -159,11 +181,11 @@ NH_DEV bool local_condense(const nh_member& m, const NodeCoef& c0, const NodeCoe
       const NodeCoef& q = *cj[j];
       double Mij = M[2 * i + j], Kij = K[2 * i + j];
       A[2 * i][2 * j] = -Kij + Mij * q.s11;
-      A[2 * i][2 * j + 1] = Mij * (q.s12 / rho);
+      A[2 * i][2 * j + 1] = Mij * (q.s12 * inv_rho);
       A[2 * i + 1][2 * j + 1] = -Kij + Mij * (-q.s11);
       A[2 * i + 1][2 * j] = Mij * (rho * q.s22);
     }
-    A[2 * i][4] = fma(M[2 * i + 1], c1.f1 / rho, M[2 * i] * (c0.f1 / rho));
+    A[2 * i][4] = fma(M[2 * i + 1], c1.f1 * inv_rho, M[2 * i] * (c0.f1 * inv_rho));
     A[2 * i + 1][4] = fma(M[2 * i + 1], c1.f2, M[2 * i] * c0.f2);
   }
   // faces (c12 = -1/2, c22 = 0): left  -Q* = -(Q0 + c11 (a - P0)),  -P* = -a
