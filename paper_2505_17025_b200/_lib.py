@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libnhswe_b200.so")
+LIB_PATH = os.environ.get("NH_LIB") or os.path.join(_HERE, "_lib", "libnhswe_b200.so")
 
 # ---- constants mirrored from the header
 BOTTOM_FLAT, BOTTOM_PLATE, BOTTOM_QUARTIC_SLIDE, BOTTOM_SMOOTH_BOX, BOTTOM_SLOPE_SLIDE = range(5)

@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(NH_STEP_MAX_THREADS) nh_solve_kernel(SolveArgs
   Super agg = chunk_aggregate<E>(Sk, tflag);
   if (tid == 0) ts.pub[6] = outer[N - 1];
   double a_in, z_in;
-  tree_solve(cluster, ts, C, rank, W, warp, lane, tflag, agg, a_in, z_in);
+  tree_solve(cluster, ts, C, rank, W, warp, lane, tflag, true, agg, a_in, z_in);
   double aprev[E], znext[E];
   chunk_unwind<E>(Sk, a_in, z_in, aprev, znext);
 #pragma unroll

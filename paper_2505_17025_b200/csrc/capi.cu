@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <mutex>
+#include <cstdlib>
 #include "step_kernel.cuh"
 
 extern "C" {
@@ -20,7 +21,16 @@ int nh_launch_momentum(const nh_member*, int, int, const double*, const double*,
 
 namespace {
 
-constexpr int kE = 3;
+constexpr int kE = 3;   // elements per thread of the coefficient-driven solve kernel
+
+int variant() {
+  static int v = [] {
+    const char* e = getenv("NH_STEP_VARIANT");
+    int x = e ? atoi(e) : 0;
+    return (x < 0 || x > 3) ? 0 : x;
+  }();
+  return v;
+}
 
 struct Plan {
   int cluster, tile, threads;
@@ -31,9 +41,21 @@ struct Plan {
 // elements plus NH_HALO on each side in shared memory; clusters are as small
 // as the 384-thread CTA allows for large ensembles (more members in flight),
 // and up to 8 CTAs for small ensembles (lower step latency).
+int max_threads() {
+  static int v = [] {
+    const char* e = getenv("NH_MAX_THREADS");
+    int cap = nh_step_variant_maxt(variant());
+    int x = e ? atoi(e) : cap;
+    if (x < 32 || x > cap) x = cap;
+    return x;
+  }();
+  return v;
+}
+
 Plan make_plan(int n, int members) {
   const int H = NH_HALO;
-  const int tile_max = kE * NH_STEP_MAX_THREADS - 2 * H;
+  const int E = nh_step_variant_E(variant());
+  const int tile_max = E * max_threads() - 2 * H;
   int cmin = (n + tile_max - 1) / tile_max;
   int c = cmin;
   if ((long long)members * cmin < 148) {
@@ -46,20 +68,21 @@ Plan make_plan(int n, int members) {
   p.cluster = c;
   p.tile = (n + c - 1) / c;
   int slots = p.tile + 2 * H;
-  int thr = (slots + kE - 1) / kE;
+  int thr = (slots + E - 1) / E;
   p.threads = std::max(32, ((thr + 31) / 32) * 32);
-  p.smem = nh_step_smem_bytes(p.threads, kE);
+  p.smem = nh_step_smem_bytes(p.threads, E);
   return p;
 }
 
 bool g_attr_done = false;
+long long* g_prof = nullptr;
 std::mutex g_attr_mu;
 
 int set_attrs() {
   std::lock_guard<std::mutex> lk(g_attr_mu);
   if (g_attr_done) return 0;
-  void* k = nh_step_kernel_ptr(kE);
-  size_t smax = nh_step_smem_bytes(NH_STEP_MAX_THREADS, kE);
+  void* k = nh_step_kernel_ptr(variant());
+  size_t smax = nh_step_smem_bytes(nh_step_variant_maxt(variant()), nh_step_variant_E(variant()));
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax) != cudaSuccess)
     return NH_E_CUDA;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
@@ -133,7 +156,8 @@ int nh_advance(const nh_member* members, int n_members, int n_elements, double* 
   a.sch = sc;
   a.B = n_members; a.N = n_elements; a.n_steps = n_steps;
   a.cluster = p.cluster; a.tile = p.tile; a.nwords = (n_elements + 31) / 32;
-  return launch_cluster(nh_step_kernel_ptr(kE), &a, n_members * p.cluster, p.threads, p.smem,
+  a.prof = g_prof;
+  return launch_cluster(nh_step_kernel_ptr(variant()), &a, n_members * p.cluster, p.threads, p.smem,
                         p.cluster, (cudaStream_t)stream);
 }
 
@@ -195,6 +219,9 @@ int nh_bottom_sample(const nh_member* members, int n_members, const double* x, i
   if (!members || n_members < 1 || n_points < 0) return NH_E_ARG;
   return nh_launch_bottom(members, n_members, x, n_points, time, out, (cudaStream_t)stream);
 }
+
+// diagnostics: device buffer [grid][NH_NPHASE] for NH_PROFILE_PHASES builds
+void nh_set_profile_buffer(long long* buf) { g_prof = buf; }
 
 const char* nh_last_cuda_error(void) { return cudaGetErrorString(cudaGetLastError()); }
 

@@ -28,6 +28,10 @@
 #include "step_kernel.cuh"
 #include "tree.cuh"
 
+#ifndef NH_STAGE_UNROLL
+#define NH_STAGE_UNROLL 1
+#endif
+
 // shared-memory field indices (SoA, each S doubles)
 enum { F_H0 = 0, F_H1, F_Q0, F_Q1, F_W0, F_W1 };
 
@@ -35,14 +39,18 @@ struct Smem {
   double* Qn;     // 6*S  state at step start -> predictor -> final state
   double* Qs;     // 6*S  stage-1 state; later phi0, phi1, dx0, dx1, hp0, hp1
   double* Fx;     // 3*T  face exchange (F1, F2L, F3) of each thread's first face
+  double* SK;     // 6*S  condensed super-element of each flagged slot
+  double* AZ;     // 2*S  (a_{e-1}, z_{e+1}) of each flagged slot after the elimination
+  short* flist;   // S    compacted list of flagged own slots
+  int* wsum;      // W+1  per-warp flagged counts (prefix)
   uint8_t* raw;   // S    raw criterion flags
   int S, T, W;
 };
 
 size_t nh_step_smem_bytes(int threads, int E) {
   int S = threads * E, W = threads / 32;
-  size_t dbl = 12 * (size_t)S + 3 * threads + W * 31 * 6 + W * 6 + W * 2 + 16 + 2 * 31 * 6;
-  return dbl * 8 + W * 4 + S + 16;
+  size_t dbl = 20 * (size_t)S + 3 * threads + W * 31 * 6 + W * 6 + W * 2 + 16 + 2 * 31 * 6;
+  return dbl * 8 + W * 4 + (W + 1) * 4 + 2 * (size_t)S + S + 32;
 }
 
 __device__ __forceinline__ double& fld(double* base, int S, int f, int j) { return base[f * S + j]; }
@@ -61,10 +69,26 @@ struct SideX {
   double sx;   // bottom slope at the node
 };
 
+#ifndef NH_KIND_TEMPLATE
+#define NH_KIND_TEMPLATE 1
+#endif
+
+// bottom evaluation specialised at compile time (KIND >= 0) or dispatched at run time
+template <int KIND, bool ALL>
+__device__ __forceinline__ Bottom6 bot(const nh_member& m, const BottomTime& bt, double x) {
+  if constexpr (KIND < 0) return bottom_eval_rt<ALL>(m, bt, x);
+  else return bottom_eval<KIND, ALL>(m, bt, x);
+}
+template <int KIND>
+__device__ __forceinline__ BottomTime bot_time(const nh_member& m, double t) {
+  if constexpr (KIND < 0) return bottom_time(m, t);
+  else return bottom_time_k<KIND>(m, t);
+}
+
 template <int KIND>
 __device__ __forceinline__ SideX load_side(const nh_member& m, const BottomTime& bt,
                                            const double* src, int S, int j, double ed, int node) {
-  Bottom6 b = bottom_eval<KIND, false>(m, bt, sample_xd(m, ed, node));
+  Bottom6 b = bot<KIND, false>(m, bt, sample_xd(m, ed, node));
   SideX r;
   r.s = make_side(src[(F_H0 + node) * S + j], src[(F_Q0 + node) * S + j],
                   src[(F_W0 + node) * S + j], b.d);
@@ -84,48 +108,49 @@ __device__ __forceinline__ double stage(const nh_member& m, double g, const doub
                                         int N, const BottomTime& bt, Fn fn) {
   const int S = sm.S;
   double speed = 0.0, sp;
-  Tend6 tend[E];
-  SideX A0 = load_side<KIND>(m, bt, src, S, j0, e0d, 0);
-  SideX A1 = load_side<KIND>(m, bt, src, S, j0, e0d, 1);
-  Face FL;
-  {
-    Side L;
-    if (e0 == 0) {
-      L = ghost_side(A0.s, m.bc_left);
-    } else {
-      int jp = j0 > 0 ? j0 - 1 : 0;
-      L = load_side<KIND>(m, bt, src, S, jp, e0d - 1.0, 1).s;
-    }
-    FL = face_flux(L, A0.s, g, sp);
-    speed = fmax(speed, sp);
+  // carried state: the previous slot's two nodes and its left face
+  SideX P0, P1;
+  Face PF;
+  Side Lprev;
+  if (e0 == 0) {
+    Lprev = load_side<KIND>(m, bt, src, S, j0, e0d, 0).s;
+    Lprev = ghost_side(Lprev, m.bc_left);
+  } else {
+    int jp = j0 > 0 ? j0 - 1 : 0;
+    Lprev = load_side<KIND>(m, bt, src, S, jp, e0d - 1.0, 1).s;
   }
-  sm.Fx[0 * sm.T + tid] = FL.F1;
-  sm.Fx[1 * sm.T + tid] = FL.F2L;
-  sm.Fx[2 * sm.T + tid] = FL.F3;
+#if NH_STAGE_UNROLL
 #pragma unroll
-  for (int k = 1; k < E; ++k) {
+#else
+#pragma unroll 1
+#endif
+  for (int k = 0; k < E; ++k) {
     SideX B0 = load_side<KIND>(m, bt, src, S, j0 + k, e0d + k, 0);
     SideX B1 = load_side<KIND>(m, bt, src, S, j0 + k, e0d + k, 1);
-    Face Fk, Fr;
-    if (e0 + k == 0) {
-      Fk = face_flux(ghost_side(B0.s, m.bc_left), B0.s, g, sp);
-    } else {
-      Fk = face_flux(A1.s, B0.s, g, sp);
-    }
+    Side L = (e0 + k == 0) ? ghost_side(B0.s, m.bc_left) : Lprev;
+    Face Fk = face_flux(L, B0.s, g, sp);
     speed = fmax(speed, sp);
-    Fr = Fk;
-    if (e0 + k - 1 == N - 1) {
-      Fr = face_flux(A1.s, ghost_side(A1.s, m.bc_right), g, sp);
-      speed = fmax(speed, sp);
+    if (k == 0) {
+      sm.Fx[0 * sm.T + tid] = Fk.F1;
+      sm.Fx[1 * sm.T + tid] = Fk.F2L;
+      sm.Fx[2 * sm.T + tid] = Fk.F3;
+    } else {
+      Face Fr = Fk;
+      if (e0 + k - 1 == N - 1) {
+        Fr = face_flux(P1.s, ghost_side(P1.s, m.bc_right), g, sp);
+        speed = fmax(speed, sp);
+      }
+      Tend6 td;
+      element_tendency(m, g, P0.s, P1.s, PF, Fr, P0.sx, P1.sx, td.v);
+      fn(k - 1, td);
     }
-    element_tendency(m, g, A0.s, A1.s, FL, Fr, A0.sx, A1.sx, tend[k - 1].v);
-    A0 = B0; A1 = B1; FL = Fk;
+    P0 = B0; P1 = B1; PF = Fk; Lprev = B1.s;
   }
   __syncthreads();
   {
     Face fr;
     if (e0 + E - 1 == N - 1) {
-      fr = face_flux(A1.s, ghost_side(A1.s, m.bc_right), g, sp);
+      fr = face_flux(P1.s, ghost_side(P1.s, m.bc_right), g, sp);
       speed = fmax(speed, sp);
     } else {
       int tn = tid + 1 < sm.T ? tid + 1 : tid;
@@ -134,10 +159,10 @@ __device__ __forceinline__ double stage(const nh_member& m, double g, const doub
       fr.F3 = sm.Fx[2 * sm.T + tn];
       fr.F2R = 0.0;
     }
-    element_tendency(m, g, A0.s, A1.s, FL, fr, A0.sx, A1.sx, tend[E - 1].v);
+    Tend6 td;
+    element_tendency(m, g, P0.s, P1.s, PF, fr, P0.sx, P1.sx, td.v);
+    fn(E - 1, td);
   }
-#pragma unroll
-  for (int k = 0; k < E; ++k) fn(k, tend[k]);
   return speed;
 }
 
@@ -174,11 +199,20 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
 
   double cfl_max = 0.0;
   long long flagged_sum = 0;
+#if NH_PROFILE_PHASES
+  long long prof[NH_NPHASE];
+#pragma unroll
+  for (int i = 0; i < NH_NPHASE; ++i) prof[i] = 0;
+  long long tlast = clock64();
+#define NH_TS(i) do { long long tc_ = clock64(); prof[i] += tc_ - tlast; tlast = tc_; } while (0)
+#else
+#define NH_TS(i) do { } while (0)
+#endif
 
   for (int step = 0; step < a.n_steps; ++step) {
     const double t1 = do_pred ? t + dt : t;
-    const BottomTime bt0 = bottom_time_k<KIND>(m, t);
-    const BottomTime bt1 = bottom_time_k<KIND>(m, t1);
+    const BottomTime bt0 = bot_time<KIND>(m, t);
+    const BottomTime bt1 = bot_time<KIND>(m, t1);
     // member-wide any(hw != 0) of this step's input (adaptivity.py:153)
     bool hw_any = true;
     if (wcrit) {
@@ -206,6 +240,7 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
       });
       if (sch.record_cfl) cfl_max = fmax(cfl_max, sp * dt / m.dx);
       __syncthreads();
+      NH_TS(0);
       // ---------------- stage 2 at t + dt: Qn += dt/2 k2 ----------------
       stage<E, KIND>(m, g, sm.Qs, sm, tid, j0, e0, e0d, N, bt1, [&](int k, const Tend6 K2) {
         const double* k2 = K2.v;
@@ -216,13 +251,18 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
             !(fld(sm.Qn, S, F_H0, j) > 0.0 && fld(sm.Qn, S, F_H1, j) > 0.0))
           nh_report(st, step, NH_ERR_POSITIVITY_STAGE2, -1);
       });
+      NH_TS(1);
     }
 
     if (do_corr) {
       // ---------------- criterion on the predictor (t+dt) ----------------
       const bool all = sch.mode == NH_MODE_GLOBAL || (wcrit && !hw_any);
       if (sch.mode == NH_MODE_ADAPTIVE && !all) {
+#if NH_STAGE_UNROLL
 #pragma unroll
+#else
+#pragma unroll 1
+#endif
         for (int k = 0; k < E; ++k) {
           int j = j0 + k, e = e0 + k;
           uint8_t fl = 0;
@@ -231,14 +271,14 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
             double v0, v1;
             switch (sch.criterion) {
               case NH_CRIT_ETA_OVER_D: {
-                double d0 = bottom_eval<KIND, false>(m, bt1, sample_xd(m, e0d + k, 0)).d;
-                double d1 = bottom_eval<KIND, false>(m, bt1, sample_xd(m, e0d + k, 1)).d;
+                double d0 = bot<KIND, false>(m, bt1, sample_xd(m, e0d + k, 0)).d;
+                double d1 = bot<KIND, false>(m, bt1, sample_xd(m, e0d + k, 1)).d;
                 v0 = fabs((h0 - d0) * nh_rcp(d0)); v1 = fabs((h1 - d1) * nh_rcp(d1));
                 break;
               }
               case NH_CRIT_ETA_X: {
-                double d0 = bottom_eval<KIND, false>(m, bt1, sample_xd(m, e0d + k, 0)).d;
-                double d1 = bottom_eval<KIND, false>(m, bt1, sample_xd(m, e0d + k, 1)).d;
+                double d0 = bot<KIND, false>(m, bt1, sample_xd(m, e0d + k, 0)).d;
+                double d1 = bot<KIND, false>(m, bt1, sample_xd(m, e0d + k, 1)).d;
                 v0 = fabs(elem_deriv(m, h0 - d0, h1 - d1, 0));
                 v1 = fabs(elem_deriv(m, h0 - d0, h1 - d1, 1));
                 break;
@@ -283,6 +323,7 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
         }
       }
       __syncthreads();
+      NH_TS(2);
       const bool enl = sch.mode == NH_MODE_ADAPTIVE && !all && sch.enlarge;
       auto eff = [&](int j) -> bool {
         int e = c0 - H + j;
@@ -295,44 +336,94 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
         return f;
       };
 
-      // ---------------- per-element condensation ----------------
-      Super Sk[E];
-      double R[E][6];
-      bool flg[E];
-      bool tflag = false;
+      // ---------------- compaction of the flagged own elements ----------------
+      // Flagged elements are spread evenly over all threads of the CTA, so a
+      // CTA with F flagged elements condenses them in ceil(F/T) rounds
+      // instead of E rounds on whichever threads happen to own them.
+      int myf = 0, nmy = 0;
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         int j = j0 + k, e = e0 + k;
-        bool own = e >= c0 && e < c1;
-        flg[k] = own && eff(j);
-        tflag = tflag || flg[k];
-        flagged_sum += flg[k] ? 1 : 0;
+        if (e >= c0 && e < c1 && eff(j)) { myf |= 1 << k; ++nmy; }
+      }
+      const bool tflag = myf != 0;
+      int incl = nmy;
 #pragma unroll
-        for (int q = 0; q < 6; ++q) R[k][q] = 0.0;
-        if (!own) {
+      for (int o = 1; o < 32; o <<= 1) {
+        int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (lane == 31) sm.wsum[warp] = incl;
+      __syncthreads();
+      if (warp == 0) {
+        int v = lane < W ? sm.wsum[lane] : 0, x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (lane < W) sm.wsum[lane] = x - v;          // exclusive warp offsets
+        if (lane == W - 1) sm.wsum[W] = x;            // total
+      }
+      __syncthreads();
+      {
+        int pos = sm.wsum[warp] + incl - nmy;
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+          if (myf & (1 << k)) sm.flist[pos++] = (short)(j0 + k);
+      }
+      const int F = sm.wsum[W];
+      flagged_sum += nmy;
+      __syncthreads();
+
+      // ---------------- condensation of the compacted elements ----------------
+      Super Sc[E];
+      double Rc[E][6];
+      int jc[E];
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        int i = r * T + tid;
+        jc[r] = i < F ? (int)sm.flist[i] : -1;
+        if (jc[r] < 0) continue;
+        const int j = jc[r], e = c0 - H + j;
+        const double ed = (double)e;
+        bool range_end = (e == N - 1) || !eff(j + 1);
+        double h0 = fld(sm.Qn, S, F_H0, j), h1 = fld(sm.Qn, S, F_H1, j);
+        Bottom6 b0 = bot<KIND, true>(m, bt1, sample_xd(m, ed, 0));
+        Bottom6 b1 = bot<KIND, true>(m, bt1, sample_xd(m, ed, 1));
+        Chan ch0{b0.d, b0.d_x, b0.d_t, b0.d_tt, b0.d_xt, b0.d_xx};
+        Chan ch1{b1.d, b1.d_x, b1.d_t, b1.d_tt, b1.d_xt, b1.d_xx};
+        NodeCoef q0 = ldg_coefficients(h0, fld(sm.Qn, S, F_Q0, j), fld(sm.Qn, S, F_W0, j),
+                                       elem_deriv(m, h0, h1, 0),
+                                       elem_deriv(m, h0 - b0.d, h1 - b1.d, 0), ch0, lk);
+        NodeCoef q1 = ldg_coefficients(h1, fld(sm.Qn, S, F_Q1, j), fld(sm.Qn, S, F_W1, j),
+                                       elem_deriv(m, h0, h1, 1),
+                                       elem_deriv(m, h0 - b0.d, h1 - b1.d, 1), ch1, lk);
+        fld(sm.Qs, S, 0, j) = q0.phi;
+        fld(sm.Qs, S, 1, j) = q1.phi;
+        fld(sm.Qs, S, 2, j) = b0.d_x;
+        fld(sm.Qs, S, 3, j) = b1.d_x;
+        bool ok = local_condense(m, q0, q1, lk.rho, lk.inv_rho, c11, range_end, Sc[r], Rc[r]);
+        if (!ok) nh_report(st, step, NH_ERR_SOLVE_PIVOT, e);
+        fld(sm.SK, S, 0, j) = Sc[r].ga; fld(sm.SK, S, 1, j) = Sc[r].aa;
+        fld(sm.SK, S, 2, j) = Sc[r].ba; fld(sm.SK, S, 3, j) = Sc[r].gz;
+        fld(sm.SK, S, 4, j) = Sc[r].az; fld(sm.SK, S, 5, j) = Sc[r].bz;
+      }
+      __syncthreads();
+      NH_TS(3);
+
+      // ---------------- elimination over the slot chain ----------------
+      Super Sk[E];
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        int j = j0 + k, e = e0 + k;
+        if (!(e >= c0 && e < c1)) {
           Sk[k] = super_identity();
-        } else if (!flg[k]) {
+        } else if (!(myf & (1 << k))) {
           Sk[k] = super_gap(fld(sm.Qn, S, F_Q0, j));
         } else {
-          bool range_end = (e == N - 1) || !eff(j + 1);
-          double h0 = fld(sm.Qn, S, F_H0, j), h1 = fld(sm.Qn, S, F_H1, j);
-          Bottom6 b0 = bottom_eval<KIND, true>(m, bt1, sample_xd(m, e0d + k, 0));
-          Bottom6 b1 = bottom_eval<KIND, true>(m, bt1, sample_xd(m, e0d + k, 1));
-          Chan ch0{b0.d, b0.d_x, b0.d_t, b0.d_tt, b0.d_xt, b0.d_xx};
-          Chan ch1{b1.d, b1.d_x, b1.d_t, b1.d_tt, b1.d_xt, b1.d_xx};
-          double hx = elem_deriv(m, h0, h1, 0);
-          double ex = elem_deriv(m, h0 - b0.d, h1 - b1.d, 0);
-          NodeCoef q0 = ldg_coefficients(h0, fld(sm.Qn, S, F_Q0, j), fld(sm.Qn, S, F_W0, j),
-                                         hx, ex, ch0, lk);
-          NodeCoef q1 = ldg_coefficients(h1, fld(sm.Qn, S, F_Q1, j), fld(sm.Qn, S, F_W1, j),
-                                         elem_deriv(m, h0, h1, 1),
-                                         elem_deriv(m, h0 - b0.d, h1 - b1.d, 1), ch1, lk);
-          fld(sm.Qs, S, 0, j) = q0.phi;
-          fld(sm.Qs, S, 1, j) = q1.phi;
-          fld(sm.Qs, S, 2, j) = b0.d_x;
-          fld(sm.Qs, S, 3, j) = b1.d_x;
-          bool ok = local_condense(m, q0, q1, lk.rho, lk.inv_rho, c11, range_end, Sk[k], R[k]);
-          if (!ok) nh_report(st, step, NH_ERR_SOLVE_PIVOT, e);
+          Sk[k] = Super{fld(sm.SK, S, 0, j), fld(sm.SK, S, 1, j), fld(sm.SK, S, 2, j),
+                        fld(sm.SK, S, 3, j), fld(sm.SK, S, 4, j), fld(sm.SK, S, 5, j)};
         }
       }
       Super agg = chunk_aggregate<E>(Sk, tflag);
@@ -343,81 +434,102 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
         ts.pub[6] = (m.bc_right == NH_BC_WALL) ? -q : q;
       }
       double a_in, z_in;
-      tree_solve(cluster, ts, C, rank, W, warp, lane, tflag, agg, a_in, z_in);
-      // chunk back-substitution and reconstruction
-      double pk[E][2];
-      const bool last_step = (step == a.n_steps - 1);
-#pragma unroll
-      for (int k = 0; k < E; ++k) { pk[k][0] = 0.0; pk[k][1] = 0.0; }
+#if NH_PROFILE_PHASES
+      prof[14] = clock64();
+      tree_solve(cluster, ts, C, rank, W, warp, lane, tflag, F > 0, agg, a_in, z_in,
+                 tid == 0 ? prof + 10 : nullptr);
+#else
+      tree_solve(cluster, ts, C, rank, W, warp, lane, tflag, F > 0, agg, a_in, z_in);
+#endif
+      NH_TS(4);
       if (tflag) {
         double aprev[E], znext[E];
         chunk_unwind<E>(Sk, a_in, z_in, aprev, znext);
 #pragma unroll
         for (int k = 0; k < E; ++k) {
-          if (!flg[k]) continue;
-          int j = j0 + k, e = e0 + k;
-          double P0, P1, Q0, Q1;
-          reconstruct(Sk[k], R[k], aprev[k], znext[k], c11, P0, P1, Q0, Q1);
-          if (!isfinite(P0 + P1 + Q0 + Q1)) nh_report(st, step, NH_ERR_SOLVE_NONFINITE, e);
-          pk[k][0] = lk.rho * P0; pk[k][1] = lk.rho * P1;
-          fld(sm.Qn, S, F_Q0, j) = Q0;
-          fld(sm.Qn, S, F_Q1, j) = Q1;
+          if (!(myf & (1 << k))) continue;
+          fld(sm.AZ, S, 0, j0 + k) = aprev[k];
+          fld(sm.AZ, S, 1, j0 + k) = znext[k];
         }
       }
+      // unflagged own slots carry p = 0
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         int j = j0 + k, e = e0 + k;
-        if (e >= c0 && e < c1) {
-          fld(sm.Qs, S, 4, j) = fld(sm.Qn, S, F_H0, j) * pk[k][0];
-          fld(sm.Qs, S, 5, j) = fld(sm.Qn, S, F_H1, j) * pk[k][1];
-          if (last_step && a.p_out) {
+        if (e >= c0 && e < c1 && !(myf & (1 << k))) {
+          fld(sm.Qs, S, 4, j) = 0.0;
+          fld(sm.Qs, S, 5, j) = 0.0;
+          if (step == a.n_steps - 1 && a.p_out) {
             size_t o = base + (size_t)e * 2;
-            a.p_out[o] = pk[k][0];
-            a.p_out[o + 1] = pk[k][1];
+            a.p_out[o] = 0.0;
+            a.p_out[o + 1] = 0.0;
           }
         }
       }
-      cluster.sync();   // ---- B3: (h p) traces visible to the neighbours
-      // hw update from the bottom pressure (corrector.py:441-482)
-      if (tflag) {
+      __syncthreads();
+      // ---------------- reconstruction of the compacted elements ----------------
+      double pk[E][2];
 #pragma unroll
-        for (int k = 0; k < E; ++k) {
-          if (!flg[k]) continue;
-          int j = j0 + k, e = e0 + k;
-          double hp0 = fld(sm.Qs, S, 4, j), hp1 = fld(sm.Qs, S, 5, j);
-          double hx0 = elem_deriv(m, hp0, hp1, 0), hx1 = elem_deriv(m, hp0, hp1, 1);
-          if (e < N - 1) {
-            double hr;
-            if (e + 1 < c1) hr = fld(sm.Qs, S, 4, j + 1);
-            else hr = dsm_read(cluster, sm.Qs + 4 * S + (e + 1 - (rank + 1) * tile + H), rank + 1);
-            double avg = 0.5 * (hp1 + hr);
-            hx0 += (avg - hp1) * m.lift_right[0];
-            hx1 += (avg - hp1) * m.lift_right[1];
-          }
-          if (e > 0) {
-            double hl;
-            if (e - 1 >= c0) hl = fld(sm.Qs, S, 5, j - 1);
-            else hl = dsm_read(cluster, sm.Qs + 5 * S + (e - 1 - (rank - 1) * tile + H), rank - 1);
-            double avg = 0.5 * (hl + hp0);
-            hx0 -= (avg - hp0) * m.lift_left[0];
-            hx1 -= (avg - hp0) * m.lift_left[1];
-          }
-          double dx0 = fld(sm.Qs, S, 2, j), dx1 = fld(sm.Qs, S, 3, j);
-          double r0 = nh_rcp(4.0 + dx0 * dx0), r1 = nh_rcp(4.0 + dx1 * dx1);
-          double bp0 = (6.0 * r0) * pk[k][0] + (dx0 * r0) * hx0 + fld(sm.Qs, S, 0, j);
-          double bp1 = (6.0 * r1) * pk[k][1] + (dx1 * r1) * hx1 + fld(sm.Qs, S, 1, j);
-          fld(sm.Qn, S, F_W0, j) += lk.cdt * bp0;
-          fld(sm.Qn, S, F_W1, j) += lk.cdt * bp1;
-          if (a.flag_bits) {
-            uint32_t* fb = a.flag_bits + ((size_t)step * a.B + b) * a.nwords;
-            atomicOr(fb + (e >> 5), 1u << (e & 31));
-          }
+      for (int r = 0; r < E; ++r) {
+        pk[r][0] = 0.0; pk[r][1] = 0.0;
+        if (jc[r] < 0) continue;
+        const int j = jc[r], e = c0 - H + j;
+        double P0, P1, Q0, Q1;
+        reconstruct(Sc[r], Rc[r], fld(sm.AZ, S, 0, j), fld(sm.AZ, S, 1, j), c11, P0, P1, Q0, Q1);
+        if (!isfinite(P0 + P1 + Q0 + Q1)) nh_report(st, step, NH_ERR_SOLVE_NONFINITE, e);
+        pk[r][0] = lk.rho * P0; pk[r][1] = lk.rho * P1;
+        fld(sm.Qn, S, F_Q0, j) = Q0;
+        fld(sm.Qn, S, F_Q1, j) = Q1;
+        fld(sm.Qs, S, 4, j) = fld(sm.Qn, S, F_H0, j) * pk[r][0];
+        fld(sm.Qs, S, 5, j) = fld(sm.Qn, S, F_H1, j) * pk[r][1];
+        if (step == a.n_steps - 1 && a.p_out) {
+          size_t o = base + (size_t)e * 2;
+          a.p_out[o] = pk[r][0];
+          a.p_out[o + 1] = pk[r][1];
+        }
+      }
+      NH_TS(5);
+      cluster.sync();   // ---- B3: (h p) traces visible to the neighbours
+      NH_TS(6);
+      // hw update from the bottom pressure (corrector.py:441-482)
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        if (jc[r] < 0) continue;
+        const int j = jc[r], e = c0 - H + j;
+        double hp0 = fld(sm.Qs, S, 4, j), hp1 = fld(sm.Qs, S, 5, j);
+        double hx0 = elem_deriv(m, hp0, hp1, 0), hx1 = elem_deriv(m, hp0, hp1, 1);
+        if (e < N - 1) {
+          double hr;
+          if (e + 1 < c1) hr = fld(sm.Qs, S, 4, j + 1);
+          else hr = dsm_read(cluster, sm.Qs + 4 * S + (e + 1 - (rank + 1) * tile + H), rank + 1);
+          double avg = 0.5 * (hp1 + hr);
+          hx0 += (avg - hp1) * m.lift_right[0];
+          hx1 += (avg - hp1) * m.lift_right[1];
+        }
+        if (e > 0) {
+          double hl;
+          if (e - 1 >= c0) hl = fld(sm.Qs, S, 5, j - 1);
+          else hl = dsm_read(cluster, sm.Qs + 5 * S + (e - 1 - (rank - 1) * tile + H), rank - 1);
+          double avg = 0.5 * (hl + hp0);
+          hx0 -= (avg - hp0) * m.lift_left[0];
+          hx1 -= (avg - hp0) * m.lift_left[1];
+        }
+        double dx0 = fld(sm.Qs, S, 2, j), dx1 = fld(sm.Qs, S, 3, j);
+        double r0 = nh_rcp(4.0 + dx0 * dx0), r1 = nh_rcp(4.0 + dx1 * dx1);
+        double bp0 = (6.0 * r0) * pk[r][0] + (dx0 * r0) * hx0 + fld(sm.Qs, S, 0, j);
+        double bp1 = (6.0 * r1) * pk[r][1] + (dx1 * r1) * hx1 + fld(sm.Qs, S, 1, j);
+        fld(sm.Qn, S, F_W0, j) += lk.cdt * bp0;
+        fld(sm.Qn, S, F_W1, j) += lk.cdt * bp1;
+        if (a.flag_bits) {
+          uint32_t* fb = a.flag_bits + ((size_t)step * a.B + b) * a.nwords;
+          atomicOr(fb + (e >> 5), 1u << (e & 31));
         }
       }
     }
 
     // ---------------- step end: halo push, member-wide any(hw) ----------------
     __syncthreads();
+    NH_TS(7);
     if (C > 1) {
       const int per = H * 6;
       for (int idx = tid; idx < 2 * per; idx += T) {
@@ -450,9 +562,17 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
       any = __syncthreads_or(any);
       if (tid == 0) ts.pub[7] = any ? 1.0 : 0.0;
     }
+    NH_TS(8);
     cluster.sync();   // ---- B1: halos and flags in place for the next step
+    NH_TS(9);
     t = t1;
   }
+#if NH_PROFILE_PHASES
+  if (tid == 0 && a.prof) {
+#pragma unroll
+    for (int i = 0; i < NH_NPHASE; ++i) a.prof[blockIdx.x * NH_NPHASE + i] = prof[i];
+  }
+#endif
 
   // ---------------- store the member tile ----------------
   for (int j = tid; j < S; j += T) {
@@ -483,8 +603,8 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
   }
 }
 
-template <int E>
-__global__ void __launch_bounds__(NH_STEP_MAX_THREADS) nh_step_kernel(StepArgs a) {
+template <int E, int MAXT>
+__global__ void __launch_bounds__(MAXT) nh_step_kernel(StepArgs a) {
   cg::cluster_group cluster = cg::this_cluster();
   const int C = a.cluster;
   const int rank = (int)cluster.block_rank();
@@ -511,8 +631,12 @@ __global__ void __launch_bounds__(NH_STEP_MAX_THREADS) nh_step_kernel(StepArgs a
   ts.pub = ts.wio + W * 2;
   ts.bnode = ts.pub + 16;
   ts.cnode = ts.bnode + 31 * 6;
-  ts.wflag = (int*)(ts.cnode + 31 * 6);
-  sm.raw = (uint8_t*)(ts.wflag + W);
+  sm.SK = ts.cnode + 31 * 6;
+  sm.AZ = sm.SK + 6 * S;
+  ts.wflag = (int*)(sm.AZ + 2 * S);
+  sm.wsum = ts.wflag + W;
+  sm.flist = (short*)(sm.wsum + W + 1);
+  sm.raw = (uint8_t*)(sm.flist + S);
 
   if (tid == 0) {
     msh = a.members[b];
@@ -546,6 +670,7 @@ __global__ void __launch_bounds__(NH_STEP_MAX_THREADS) nh_step_kernel(StepArgs a
     if (tid == 0) { ts.pub[7] = any ? 1.0 : 0.0; ts.pub[6] = 0.0; }
   }
   cluster.sync();
+#if NH_KIND_TEMPLATE
   switch (msh.bottom_kind) {
     case NH_BOTTOM_FLAT: member_steps<E, NH_BOTTOM_FLAT>(a, cluster, msh, sm, ts, ksh, t); break;
     case NH_BOTTOM_PLATE: member_steps<E, NH_BOTTOM_PLATE>(a, cluster, msh, sm, ts, ksh, t); break;
@@ -556,8 +681,24 @@ __global__ void __launch_bounds__(NH_STEP_MAX_THREADS) nh_step_kernel(StepArgs a
     default:
       member_steps<E, NH_BOTTOM_SLOPE_SLIDE>(a, cluster, msh, sm, ts, ksh, t); break;
   }
+#else
+  member_steps<E, -1>(a, cluster, msh, sm, ts, ksh, t);
+#endif
 }
 
-template __global__ void nh_step_kernel<3>(StepArgs);
+template __global__ void nh_step_kernel<3, 384>(StepArgs);
+template __global__ void nh_step_kernel<1, 1024>(StepArgs);
+template __global__ void nh_step_kernel<1, 512>(StepArgs);
+template __global__ void nh_step_kernel<2, 512>(StepArgs);
 
-void* nh_step_kernel_ptr(int E) { return E == 3 ? (void*)nh_step_kernel<3> : nullptr; }
+// variants: 0 = (E 3, <=384 threads), 1 = (E 1, <=1024), 2 = (E 1, <=512), 3 = (E 2, <=512)
+void* nh_step_kernel_ptr(int v) {
+  switch (v) {
+    case 1: return (void*)nh_step_kernel<1, 1024>;
+    case 2: return (void*)nh_step_kernel<1, 512>;
+    case 3: return (void*)nh_step_kernel<2, 512>;
+    default: return (void*)nh_step_kernel<3, 384>;
+  }
+}
+int nh_step_variant_E(int v) { return v == 1 || v == 2 ? 1 : v == 3 ? 2 : 3; }
+int nh_step_variant_maxt(int v) { return v == 1 ? 1024 : v == 2 || v == 3 ? 512 : 384; }

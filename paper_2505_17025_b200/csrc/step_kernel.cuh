@@ -21,7 +21,10 @@ struct StepArgs {
   nh_scheme sch;
   int B, N, n_steps;
   int cluster, tile, nwords;
+  long long* prof;   // NH_PROFILE_PHASES builds: [grid][NH_NPHASE] cycle sums (else unused)
 };
+
+#define NH_NPHASE 15
 
 struct SolveArgs {
   const nh_member* members;
@@ -37,5 +40,7 @@ struct SolveArgs {
 
 size_t nh_step_smem_bytes(int threads, int E);
 size_t nh_solve_smem_bytes(int threads);
-void* nh_step_kernel_ptr(int E);
+void* nh_step_kernel_ptr(int variant);
+int nh_step_variant_E(int variant);
+int nh_step_variant_maxt(int variant);
 void* nh_solve_kernel_ptr(int E);

@@ -102,7 +102,9 @@ __device__ __forceinline__ int tree_levels(int n) {
 // pub[6] (right ghost) must be set by its owner before the call.
 __device__ __forceinline__ void tree_solve(cg::cluster_group& cluster, const TreeSmem& ts, int C,
                                            int rank, int W, int warp, int lane, bool tflag,
-                                           Super agg, double& a_in, double& z_in) {
+                                           bool cta_any, Super agg, double& a_in, double& z_in,
+                                           long long* tprof = nullptr) {
+#define NH_TT(i) do { if (tprof) { long long c_ = clock64(); tprof[i] += c_ - tprof[4]; tprof[4] = c_; } } while (0)
   double* wn = ts.wnode + warp * 31 * 6;
   const bool wany = __any_sync(0xffffffffu, tflag);
   if (wany) {
@@ -120,6 +122,7 @@ __device__ __forceinline__ void tree_solve(cg::cluster_group& cluster, const Tre
     ts.wflag[warp] = wany ? 1 : 0;
   }
   __syncthreads();
+  NH_TT(0);
   const int lb = tree_levels(W), lc = tree_levels(C);
   if (warp == 0) {
     Super v = super_identity();
@@ -127,14 +130,17 @@ __device__ __forceinline__ void tree_solve(cg::cluster_group& cluster, const Tre
       const double* wa = ts.wagg + lane * 6;
       v = Super{wa[0], wa[1], wa[2], wa[3], wa[4], wa[5]};
     }
-    v = warp_up(v, ts.bnode, lane, lb);
+    // a CTA without flagged elements is the gap of its first element: no merges
+    if (cta_any) v = warp_up(v, ts.bnode, lane, lb);
     if (lane == 0) {
       ts.pub[0] = v.ga; ts.pub[1] = v.aa; ts.pub[2] = v.ba;
       ts.pub[3] = v.gz; ts.pub[4] = v.az; ts.pub[5] = v.bz;
     }
   }
+  NH_TT(1);
   cluster.sync();   // CTA aggregates (and the right ghost) visible cluster-wide
-  if (warp == 0) {
+  NH_TT(2);
+  if (warp == 0 && cta_any) {
     Super v = super_identity();
     if (lane < C) {
       const double* rp = cluster.map_shared_rank(ts.pub, lane);
@@ -154,9 +160,12 @@ __device__ __forceinline__ void tree_solve(cg::cluster_group& cluster, const Tre
     }
   }
   __syncthreads();
+  NH_TT(3);
+  if (!cta_any) { a_in = 0.0; z_in = 0.0; return; }
   a_in = ts.wio[warp * 2 + 0];
   z_in = ts.wio[warp * 2 + 1];
   if (wany) warp_down(a_in, z_in, wn, lane, 5);
+#undef NH_TT
 }
 
 // Chunk back-substitution: given the chunk's (a_in, z_in) and its elements'
