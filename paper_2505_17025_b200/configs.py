@@ -217,7 +217,7 @@ def _slide_ok(tan_t, A, sigma, x0, xs):
     x_stop = 0.7 / tan_t
     ok = x_stop >= x0 + 0.5
     worst = np.full(tan_t.shape, np.inf)
-    for f in np.linspace(0.0, 1.0, 16):
+    for f in np.linspace(0.0, 1.0, 9):
         xc = x0 + f * np.maximum(x_stop - x0, 0.0)
         r = (xs[None, :] - xc[:, None]) / sigma[:, None]
         d = np.minimum(0.1 + xs[None, :] * tan_t[:, None], 1.0) - A[:, None] * np.exp(-0.5 * r * r)
@@ -229,7 +229,7 @@ def _slide_ok(tan_t, A, sigma, x0, xs):
 def _config5_table(n_members: int, seed: int):
     """(tan_theta, A, sigma, x0, u_t) per member, rejection-sampled in rounds."""
     rng = np.random.default_rng(seed)
-    xs = np.linspace(0.0, 20.0, 801)
+    xs = np.linspace(0.0, 20.0, 321)
     out = np.zeros((n_members, 5))
     todo = np.arange(n_members)
     for _ in range(200):

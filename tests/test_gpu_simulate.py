@@ -7,7 +7,7 @@ import pytest
 import paper_2505_17025_b200 as P
 from paper_2505_17025_b200 import configs
 from oracle import nhswe_oracle as O
-from tests.helpers import oracle_depth, oracle_member, rel
+from tests.helpers import mask_mismatch_outside_margin, oracle_depth, oracle_member, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -99,3 +99,51 @@ def test_ensemble_mixed_members():
         assert rel(gh[i] - m.bathymetry.h0, r.h - m.bathymetry.h0) <= 1e-9, i
         assert rel(gq[i], r.hu) <= 1e-9, i
         assert abs(st["flagged"][i] / (cfg.n_steps * cfg.n_elements) - r.fraction_mean) < 1e-3
+
+
+@pytest.mark.parametrize("cfg_name,members,n_steps", [("config4", (0, 1, 2047, 4095), 200),
+                                                      ("config5", (0, 65535), 40)])
+def test_sampled_ensemble_members_full_size(cfg_name, members, n_steps):
+    """Sampled members of the throughput configs at full N, stepped inside the
+    batched ensemble path, against the oracle run of the same members."""
+    cfg = configs.Config4() if cfg_name == "config4" else configs.Config5()
+    idx = list(members)
+    recs = cfg.records(idx)
+    states = [cfg.host_state(i, oracle_depth) for i in idx]
+    H, Q, W = (np.stack([s[k] for s in states]) for k in range(3))
+    ens = P.Ensemble.from_host(recs, H, Q, W)
+    mode = "adaptive"
+    ens.advance(n_steps, mode, P.Criterion("eta_over_d"))
+    st = ens.check()
+    gh, gq, gw = (x.cpu().numpy() for x in (ens.h, ens.hu, ens.hw))
+    for k, i in enumerate(idx):
+        m = cfg.member(i)
+        r = O.run(oracle_member(m.grid, m.bathymetry, m.bcs, m.dt), H[k], Q[k], W[k], n_steps,
+                  mode=mode)
+        d = oracle_depth(m.bathymetry, m.grid.sample_nodes, r.t)
+        assert rel(gh[k] - d, r.h - d) <= 1e-9, (cfg_name, i)
+        assert rel(gq[k], r.hu) <= 1e-9 or np.abs(gq[k] - r.hu).max() < 1e-12, (cfg_name, i)
+        assert abs(st["flagged"][k] / (n_steps * cfg.n_elements) - r.fraction_mean) < 1e-3
+
+
+def test_per_step_replay_after_long_run():
+    """GPU state at step n -> one oracle step vs one GPU step."""
+    cfg = configs.config1()
+    m = cfg.member(0)
+    h, hu, hw = cfg.host_state(0, None)
+    ens = P.Ensemble.from_host(cfg.records(), h[None], hu[None], hw[None])
+    crit = P.Criterion("eta_over_d")
+    ens.advance(1500, "adaptive", crit)
+    ens.check()
+    t = float(ens.time.item())
+    gh, gq, gw = (x[0].cpu().numpy() for x in (ens.h, ens.hu, ens.hw))
+    st = P.FlowState(P.NodalField(m.grid, gh), P.NodalField(m.grid, gq), P.NodalField(m.grid, gw), t)
+    r = P.adaptive_step(st, m.dt, m.bathymetry, m.bcs, mode="adaptive", crit=crit)
+    mem = oracle_member(m.grid, m.bathymetry, m.bcs, m.dt)
+    ph, pq, pw = O.heun(mem.grid, mem.bottom, mem.bcs, 9.81, gh, gq, gw, t, m.dt, cfl_warn=False)
+    o = O.step(mem, gh, gq, gw, t, "adaptive", cfl_warn=False)
+    vals = O.indicator(mem.grid, mem.bottom, "eta_over_d", ph, pq, pw, t + m.dt)
+    bad = mask_mismatch_outside_margin(r.mask.flags, vals, 1e-3)
+    assert bad.size == 0
+    assert rel(r.state.h.values - 1.0, o.h - 1.0) <= 1e-12
+    assert rel(r.state.hu.values, o.hu) <= 1e-12
