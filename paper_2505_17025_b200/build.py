@@ -21,6 +21,10 @@ SOURCES = ["capi.cu", "step_kernel.cu", "aux_kernels.cu"]
 HEADERS = ["nh_common.cuh", "bathy.cuh", "physics.cuh", "tree.cuh", "step_kernel.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "--extended-lambda", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+# default build: reference-faithful arithmetic (NH_STRICT=1, no implicit FMA contraction);
+# "fast" builds drop both (see csrc/nh_common.cuh)
+STRICT_FLAGS = ["-DNH_STRICT=1"]
+FAST_FLAGS = ["-DNH_STRICT=0", "-fmad=true"]
 
 
 def _nvcc():
@@ -40,7 +44,7 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None,
-          defines: tuple = ()) -> str:
+          defines: tuple = (), fast: bool = False) -> str:
     lib = out or LIB
     if not force and out is None and not _stale():
         return LIB
@@ -48,7 +52,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     objs = []
     for src in SOURCES:
         obj = os.path.join(os.path.dirname(lib), src.replace(".cu", ".o"))
-        cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c",
+        cmd = [_nvcc(), *NVCC_FLAGS, *(FAST_FLAGS if fast else STRICT_FLAGS),
+               *[f"-D{d}" for d in defines], "-c",
                os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

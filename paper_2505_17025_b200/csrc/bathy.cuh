@@ -110,7 +110,7 @@ __device__ __forceinline__ Bottom6 bottom_eval(const nh_member& m, const BottomT
   if (KIND == NH_BOTTOM_PLATE) {
     if (fabs(x) < p[2]) {
       double a = p[3], decay = bt.a;
-      b.d = p[0] - p[1] * (1.0 - decay);
+      b.d = RSUB(p[0], RMUL(p[1], RSUB(1.0, decay)));
       if (NEED_ALL) {
         b.d_t = -p[1] * a * decay;
         b.d_tt = p[1] * a * a * decay;
@@ -118,12 +118,16 @@ __device__ __forceinline__ Bottom6 bottom_eval(const nh_member& m, const BottomT
     }
   } else if (KIND == NH_BOTTOM_QUARTIC_SLIDE) {
     double c = p[9];
-    double xi = (x - bt.a) * c;
+    double xi = RDIV(RMUL(2.0, RSUB(x, bt.a)), p[2]);
     if (fabs(xi) < 1.0) {
       double Hs = p[1], sp = bt.b, spp = bt.c;
-      double x2 = xi * xi, x3 = x2 * xi;
-      b.d = p[0] - Hs * (1.0 - x2 * x2);
-      b.d_x = Hs * 4.0 * x3 * c;
+#if NH_STRICT
+      double x2 = RMUL(xi, xi), x3 = pow(xi, 3.0), x4 = pow(xi, 4.0);
+#else
+      double x2 = xi * xi, x3 = x2 * xi, x4 = x2 * x2;
+#endif
+      b.d = RSUB(p[0], RMUL(Hs, RSUB(1.0, x4)));
+      b.d_x = RMUL(RMUL(RMUL(Hs, 4.0), x3), c);
       if (NEED_ALL) {
         b.d_xx = Hs * 12.0 * x2 * c * c;
         b.d_t = Hs * 4.0 * x3 * (-c * sp);
@@ -133,23 +137,23 @@ __device__ __forceinline__ Bottom6 bottom_eval(const nh_member& m, const BottomT
       }
     }
   } else if (KIND == NH_BOTTOM_SMOOTH_BOX) {
-    double y = (fabs(x) - p[2]) * p[5];
+    double y = RDIV(RSUB(fabs(x), p[2]), p[4]);
     if (y < NH_BOX_YCUT) {
       double decay = bt.a, z0 = p[1], al = p[3];
-      double zeta = z0 * (1.0 - decay);
-      double E = exp(-2.0 * fabs(y));
-      double inv1 = nh_rcp(1.0 + E);
-      double S = y >= 0.0 ? E * inv1 : inv1;
+      double zeta = RMUL(z0, RSUB(1.0, decay));
+      double E = exp(RMUL(-2.0, fabs(y)));
+      double inv1 = RDIV(1.0, RADD(1.0, E));
+      double S = y >= 0.0 ? RMUL(E, inv1) : inv1;
       double sg = x >= 0.0 ? 1.0 : -1.0;
-      double sech2 = 4.0 * E * inv1 * inv1;
-      double Sx = -0.5 * sech2 * sg * p[5];
-      b.d = p[0] - zeta * S;
-      b.d_x = -zeta * Sx;
+      double sech2 = RMUL(RMUL(RMUL(4.0, E), inv1), inv1);
+      double Sx = RDIV(RMUL(RMUL(-0.5, sech2), sg), p[4]);
+      b.d = RSUB(p[0], RMUL(zeta, S));
+      b.d_x = RMUL(-zeta, Sx);
       if (NEED_ALL) {
         double zt = z0 * al * decay;
         double ztt = -z0 * al * al * decay;
         double th = (y >= 0.0 ? 1.0 : -1.0) * (1.0 - E) * inv1;
-        double Sxx = sech2 * th * p[6];
+        double Sxx = RDIV(RMUL(sech2, th), RMUL(p[4], p[4]));
         b.d_t = -zt * S;
         b.d_tt = -ztt * S;
         b.d_xt = -zt * Sx;
@@ -157,18 +161,18 @@ __device__ __forceinline__ Bottom6 bottom_eval(const nh_member& m, const BottomT
       }
     }
   } else if (KIND == NH_BOTTOM_SLOPE_SLIDE) {
-    double ramp = p[0] + x * p[1];
+    double ramp = RADD(p[0], RMUL(x, p[1]));
     bool on = ramp < p[2];
     b.d = on ? ramp : p[2];
     b.d_x = on ? p[1] : 0.0;
-    double r = (x - bt.a) * p[11];
+    double r = RDIV(RSUB(x, bt.a), p[4]);
     if (fabs(r) < NH_SLIDE_RCUT) {
-      double G = p[3] * exp(-0.5 * r * r);
-      double Gx = -G * r * p[11];
-      b.d = b.d - G;
-      b.d_x = b.d_x - Gx;
+      double G = RMUL(p[3], exp(RMUL(RMUL(-0.5, r), r)));
+      double Gx = RDIV(RMUL(-G, r), p[4]);
+      b.d = RSUB(b.d, G);
+      b.d_x = RSUB(b.d_x, Gx);
       if (NEED_ALL) {
-        double Gxx = G * (r * r - 1.0) * (p[11] * p[11]);
+        double Gxx = RDIV(RMUL(G, RSUB(RMUL(r, r), 1.0)), RMUL(p[4], p[4]));
         double v = bt.b, acc = bt.c;
         b.d_t = Gx * v;
         b.d_tt = -Gxx * v * v + Gx * acc;

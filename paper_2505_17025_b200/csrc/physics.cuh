@@ -35,8 +35,12 @@ struct Side {
 NH_DEV Side make_side(double h, double hu, double hw, double d) {
   Side s;
   s.h = h; s.hu = hu; s.hw = hw; s.d = d;
+#if NH_STRICT
+  s.rh = 0.0;
+#else
   s.rh = nh_rcp(h);
-  s.u = hu * s.rh;
+#endif
+  s.u = RDIV(hu, h);
   return s;
 }
 
@@ -52,50 +56,58 @@ NH_DEV Side ghost_side(const Side& in, int bc) {
 NH_DEV Face face_flux(const Side& L, const Side& R, double g, double& speed) {
   const double hg = 0.5 * g;
   double dm = fmin(L.d, R.d);
-  double hLs = fmax(L.h - (L.d - dm), 0.0);
-  double hRs = fmax(R.h - (R.d - dm), 0.0);
-  double cL = hg * (L.h * L.h - hLs * hLs);
-  double cR = hg * (R.h * R.h - hRs * hRs);
-  double aL = fabs(L.u) + nh_sqrt(g * hLs);
-  double aR = fabs(R.u) + nh_sqrt(g * hRs);
+  double hLs = fmax(RSUB(L.h, RSUB(L.d, dm)), 0.0);
+  double hRs = fmax(RSUB(R.h, RSUB(R.d, dm)), 0.0);
+  double cL = RMUL(hg, RSUB(RMUL(L.h, L.h), RMUL(hLs, hLs)));
+  double cR = RMUL(hg, RSUB(RMUL(R.h, R.h), RMUL(hRs, hRs)));
+  double aL = RADD(fabs(L.u), RSQRT(RMUL(g, hLs)));
+  double aR = RADD(fabs(R.u), RSQRT(RMUL(g, hRs)));
   speed = fmax(aL, aR);
-  double lam = 0.5 * speed;
-  double qL = hLs * L.u, qR = hRs * R.u;
+  double lam = RMUL(0.5, speed);
+  double qL = RMUL(hLs, L.u), qR = RMUL(hRs, R.u);
   Face f;
-  f.F1 = 0.5 * (qL + qR) - lam * (hRs - hLs);
-  double F2 = 0.5 * (qL * L.u + qR * R.u + hg * (hLs * hLs + hRs * hRs)) - lam * (qR - qL);
+  f.F1 = RSUB(RMUL(0.5, RADD(qL, qR)), RMUL(lam, RSUB(hRs, hLs)));
+  double s2 = RADD(RADD(RMUL(qL, L.u), RMUL(qR, R.u)), RMUL(hg, RADD(RMUL(hLs, hLs), RMUL(hRs, hRs))));
+  double F2 = RSUB(RMUL(0.5, s2), RMUL(lam, RSUB(qR, qL)));
+#if NH_STRICT
+  // (hLs / hL) hwL is exactly hwL when hLs == hL (IEEE x / x == 1)
+  double wL = (hLs == L.h) ? L.hw : RMUL(RDIV(hLs, L.h), L.hw);
+  double wR = (hRs == R.h) ? R.hw : RMUL(RDIV(hRs, R.h), R.hw);
+#else
   double wL = (hLs == L.h) ? L.hw : (hLs * L.rh) * L.hw;
   double wR = (hRs == R.h) ? R.hw : (hRs * R.rh) * R.hw;
-  f.F3 = 0.5 * (wL * L.u + wR * R.u) - lam * (wR - wL);
-  f.F2L = F2 + cL;
-  f.F2R = F2 + cR;
+#endif
+  f.F3 = RSUB(RMUL(0.5, RADD(RMUL(wL, L.u), RMUL(wR, R.u))), RMUL(lam, RSUB(wR, wL)));
+  f.F2L = RADD(F2, cL);
+  f.F2R = RADD(F2, cR);
   return f;
 }
 
 // Tendency of one element (hydrostatic.py:162-183).  n0/n1 = own nodes,
 // fl = face at its left, fr = face at its right, dx0/dx1 = bottom slope.
+// The volume products keep numpy's dgemm rounding: fma(v1, W1, v0*W0).
 NH_DEV void element_tendency(const nh_member& m, double g, const Side& n0, const Side& n1,
                              const Face& fl, const Face& fr, double dx0, double dx1,
                              double t[6]) {
   const double hg = 0.5 * g;
-  double f20 = n0.hu * n0.u + (hg * n0.h) * n0.h;
-  double f21 = n1.hu * n1.u + (hg * n1.h) * n1.h;
-  double f30 = n0.u * n0.hw, f31 = n1.u * n1.hw;
+  double f20 = RADD(RMUL(n0.hu, n0.u), RMUL(RMUL(hg, n0.h), n0.h));
+  double f21 = RADD(RMUL(n1.hu, n1.u), RMUL(RMUL(hg, n1.h), n1.h));
+  double f30 = RMUL(n0.u, n0.hw), f31 = RMUL(n1.u, n1.hw);
   const double* W = m.weak_div;
   const double* lr = m.lift_right;
   const double* ll = m.lift_left;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    double v1 = fma(n1.hu, W[2 * i + 1], n0.hu * W[2 * i]);
-    v1 = v1 - fr.F1 * lr[i];
-    t[0 + i] = v1 + fl.F1 * ll[i];
-    double v2 = fma(f21, W[2 * i + 1], f20 * W[2 * i]);
-    v2 = v2 - fr.F2L * lr[i];
-    v2 = v2 + fl.F2R * ll[i];
-    t[2 + i] = v2 + (g * (i ? n1.h : n0.h)) * (i ? dx1 : dx0);
-    double v3 = fma(f31, W[2 * i + 1], f30 * W[2 * i]);
-    v3 = v3 - fr.F3 * lr[i];
-    t[4 + i] = v3 + fl.F3 * ll[i];
+    double v1 = fma(n1.hu, W[2 * i + 1], RMUL(n0.hu, W[2 * i]));
+    v1 = RSUB(v1, RMUL(fr.F1, lr[i]));
+    t[0 + i] = RADD(v1, RMUL(fl.F1, ll[i]));
+    double v2 = fma(f21, W[2 * i + 1], RMUL(f20, W[2 * i]));
+    v2 = RSUB(v2, RMUL(fr.F2L, lr[i]));
+    v2 = RADD(v2, RMUL(fl.F2R, ll[i]));
+    t[2 + i] = RADD(v2, RMUL(RMUL(g, i ? n1.h : n0.h), i ? dx1 : dx0));
+    double v3 = fma(f31, W[2 * i + 1], RMUL(f30, W[2 * i]));
+    v3 = RSUB(v3, RMUL(fr.F3, lr[i]));
+    t[4 + i] = RADD(v3, RMUL(fl.F3, ll[i]));
   }
 }
 
@@ -137,7 +149,7 @@ NH_DEV NodeCoef ldg_coefficients(double h, double hu, double hw, double h_x, dou
   acc = acc + (-2.0 * u * b.d_xt - u * u * b.d_xx);
   acc = acc + (k.g * b.d_x) * eta_x;
   double quad = 4.0 + b.d_x * b.d_x;
-  c.phi = (k.rho * h * nh_rcp(quad)) * acc;
+  c.phi = nh_div(k.rho * h, quad) * acc;
   c.s22 = k.s22c * ih;
   c.s11 = (h_x - 1.5 * b.d_x) * ih;
   c.s12 = k.s12c * quad * ih;

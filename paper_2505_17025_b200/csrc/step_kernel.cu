@@ -55,9 +55,9 @@ size_t nh_step_smem_bytes(int threads, int E) {
 
 __device__ __forceinline__ double& fld(double* base, int S, int f, int j) { return base[f * S + j]; }
 
-// element derivative (grid.py:214-215) of a P1 pair, node i
+// element derivative (grid.py:214-215) of a P1 pair, node i (numpy dgemm rounding)
 __device__ __forceinline__ double elem_deriv(const nh_member& m, double v0, double v1, int i) {
-  return fma(v1, m.deriv_ref[2 * i + 1], v0 * m.deriv_ref[2 * i]) * m.two_over_dx;
+  return RMUL(fma(v1, m.deriv_ref[2 * i + 1], RMUL(v0, m.deriv_ref[2 * i])), m.two_over_dx);
 }
 
 struct Tend6 {
@@ -221,7 +221,7 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
     }
 
     if (do_pred) {
-      // ---------------- stage 1 at t: Qs = Q*, Qn += dt/2 k1 ----------------
+      // ---------------- stage 1 at t: Qs = Q* = Qn + dt k1, k1 parked in SK ----------------
       double sp = stage<E, KIND>(m, g, sm.Qn, sm, tid, j0, e0, e0d, N, bt0,
                                  [&](int k, const Tend6 K1) {
         const double* k1 = K1.v;
@@ -231,9 +231,8 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
         if (own && (hn0 <= 0.0 || hn1 <= 0.0)) nh_report(st, step, NH_ERR_POSITIVITY_ENTRY, e);
 #pragma unroll
         for (int f = 0; f < 6; ++f) {
-          double q = fld(sm.Qn, S, f, j);
-          fld(sm.Qs, S, f, j) = q + dt * k1[f];
-          fld(sm.Qn, S, f, j) = q + hdt * k1[f];
+          fld(sm.Qs, S, f, j) = RADD(fld(sm.Qn, S, f, j), RMUL(dt, k1[f]));
+          fld(sm.SK, S, f, j) = k1[f];
         }
         if (own && !(fld(sm.Qs, S, F_H0, j) > 0.0 && fld(sm.Qs, S, F_H1, j) > 0.0))
           nh_report(st, step, NH_ERR_POSITIVITY_STAGE1, -1);
@@ -241,12 +240,14 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
       if (sch.record_cfl) cfl_max = fmax(cfl_max, sp * dt / m.dx);
       __syncthreads();
       NH_TS(0);
-      // ---------------- stage 2 at t + dt: Qn += dt/2 k2 ----------------
+      // ---------------- stage 2 at t + dt: Qn = Qn + dt (k1 + k2)/2 (hydrostatic.py:208-209)
       stage<E, KIND>(m, g, sm.Qs, sm, tid, j0, e0, e0d, N, bt1, [&](int k, const Tend6 K2) {
         const double* k2 = K2.v;
         int j = j0 + k, e = e0 + k;
 #pragma unroll
-        for (int f = 0; f < 6; ++f) fld(sm.Qn, S, f, j) += hdt * k2[f];
+        for (int f = 0; f < 6; ++f)
+          fld(sm.Qn, S, f, j) =
+              RADD(fld(sm.Qn, S, f, j), RMUL(dt, RMUL(0.5, RADD(fld(sm.SK, S, f, j), k2[f]))));
         if (e >= c0 && e < c1 &&
             !(fld(sm.Qn, S, F_H0, j) > 0.0 && fld(sm.Qn, S, F_H1, j) > 0.0))
           nh_report(st, step, NH_ERR_POSITIVITY_STAGE2, -1);
@@ -273,33 +274,33 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
               case NH_CRIT_ETA_OVER_D: {
                 double d0 = bot<KIND, false>(m, bt1, sample_xd(m, e0d + k, 0)).d;
                 double d1 = bot<KIND, false>(m, bt1, sample_xd(m, e0d + k, 1)).d;
-                v0 = fabs((h0 - d0) * nh_rcp(d0)); v1 = fabs((h1 - d1) * nh_rcp(d1));
+                v0 = fabs(RDIV(RSUB(h0, d0), d0)); v1 = fabs(RDIV(RSUB(h1, d1), d1));
                 break;
               }
               case NH_CRIT_ETA_X: {
                 double d0 = bot<KIND, false>(m, bt1, sample_xd(m, e0d + k, 0)).d;
                 double d1 = bot<KIND, false>(m, bt1, sample_xd(m, e0d + k, 1)).d;
-                v0 = fabs(elem_deriv(m, h0 - d0, h1 - d1, 0));
-                v1 = fabs(elem_deriv(m, h0 - d0, h1 - d1, 1));
+                v0 = fabs(elem_deriv(m, RSUB(h0, d0), RSUB(h1, d1), 0));
+                v1 = fabs(elem_deriv(m, RSUB(h0, d0), RSUB(h1, d1), 1));
                 break;
               }
               case NH_CRIT_U:
-                v0 = fabs(fld(sm.Qn, S, F_Q0, j) * nh_rcp(h0));
-                v1 = fabs(fld(sm.Qn, S, F_Q1, j) * nh_rcp(h1));
+                v0 = fabs(RDIV(fld(sm.Qn, S, F_Q0, j), h0));
+                v1 = fabs(RDIV(fld(sm.Qn, S, F_Q1, j), h1));
                 break;
               case NH_CRIT_U_X: {
-                double u0 = fld(sm.Qn, S, F_Q0, j) * nh_rcp(h0);
-                double u1 = fld(sm.Qn, S, F_Q1, j) * nh_rcp(h1);
+                double u0 = RDIV(fld(sm.Qn, S, F_Q0, j), h0);
+                double u1 = RDIV(fld(sm.Qn, S, F_Q1, j), h1);
                 v0 = fabs(elem_deriv(m, u0, u1, 0)); v1 = fabs(elem_deriv(m, u0, u1, 1));
                 break;
               }
               case NH_CRIT_W:
-                v0 = fabs(fld(sm.Qn, S, F_W0, j) * nh_rcp(h0));
-                v1 = fabs(fld(sm.Qn, S, F_W1, j) * nh_rcp(h1));
+                v0 = fabs(RDIV(fld(sm.Qn, S, F_W0, j), h0));
+                v1 = fabs(RDIV(fld(sm.Qn, S, F_W1, j), h1));
                 break;
               default: {
-                double w0 = fld(sm.Qn, S, F_W0, j) * nh_rcp(h0);
-                double w1 = fld(sm.Qn, S, F_W1, j) * nh_rcp(h1);
+                double w0 = RDIV(fld(sm.Qn, S, F_W0, j), h0);
+                double w1 = RDIV(fld(sm.Qn, S, F_W1, j), h1);
                 v0 = fabs(elem_deriv(m, w0, w1, 0)); v1 = fabs(elem_deriv(m, w0, w1, 1));
                 break;
               }
@@ -515,9 +516,9 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
           hx1 -= (avg - hp0) * m.lift_left[1];
         }
         double dx0 = fld(sm.Qs, S, 2, j), dx1 = fld(sm.Qs, S, 3, j);
-        double r0 = nh_rcp(4.0 + dx0 * dx0), r1 = nh_rcp(4.0 + dx1 * dx1);
-        double bp0 = (6.0 * r0) * pk[r][0] + (dx0 * r0) * hx0 + fld(sm.Qs, S, 0, j);
-        double bp1 = (6.0 * r1) * pk[r][1] + (dx1 * r1) * hx1 + fld(sm.Qs, S, 1, j);
+        double q0 = 4.0 + dx0 * dx0, q1 = 4.0 + dx1 * dx1;
+        double bp0 = nh_div(6.0, q0) * pk[r][0] + nh_div(dx0, q0) * hx0 + fld(sm.Qs, S, 0, j);
+        double bp1 = nh_div(6.0, q1) * pk[r][1] + nh_div(dx1, q1) * hx1 + fld(sm.Qs, S, 1, j);
         fld(sm.Qn, S, F_W0, j) += lk.cdt * bp0;
         fld(sm.Qn, S, F_W1, j) += lk.cdt * bp1;
         if (a.flag_bits) {
