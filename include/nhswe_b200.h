@@ -18,6 +18,7 @@
 #ifndef NHSWE_B200_H
 #define NHSWE_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -130,6 +131,20 @@ int nh_advance(const nh_member* members, int n_members, int n_elements,
                double* h, double* hu, double* hw, double* time, int n_steps,
                const nh_scheme* scheme, const nh_outputs* outputs,
                nh_status* status, void* stream);
+
+/* Streaming variant of nh_advance for large ensembles (same contract and
+ * in-place semantics; modes HYDROSTATIC / GLOBAL / ADAPTIVE with the
+ * eta_over_d, eta_x, u, u_x criteria).  Every step is three kernels over
+ * independent 248-element tiles (predictor+criterion+condensation, per-member
+ * tile chain, reconstruction) with the vertical-momentum update fused into
+ * the next step's load; state goes through HBM once per step.  `workspace`
+ * is device memory of at least nh_stream_workspace_bytes(B, N) bytes. */
+int nh_stream_advance(const nh_member* members, int n_members, int n_elements,
+                      double* h, double* hu, double* hw, double* time, int n_steps,
+                      const nh_scheme* scheme, const nh_outputs* outputs,
+                      nh_status* status, void* workspace, size_t workspace_bytes,
+                      void* stream);
+size_t nh_stream_workspace_bytes(int n_members, int n_elements);
 
 /* Semi-discrete tendency, hydrostatic.rhs_operator (hydrostatic.py:88-184).
  * Outputs t_h, t_hu, t_hw [B][N][2]. */

@@ -175,10 +175,28 @@ def scheme(mode: int, kind: str = "eta_over_d", k_nh: float = 1e-3, enlarge: boo
 
 def advance(members, h, hu, hw, time, n_steps, sch, status, flag_bits=None, p_out=None,
             given=None):
-    """Enqueue nh_advance on the current stream (device tensors in, in place)."""
+    """Enqueue nh_advance (resident cluster kernel) on the current stream, in place."""
     lib = require_cuda()
     B, N = h.shape[0], h.shape[1]
     out = _lib.Outputs(ptr(flag_bits), ptr(p_out), ptr(given))
     rc = lib.nh_advance(ptr(members), B, N, ptr(h), ptr(hu), ptr(hw), ptr(time), int(n_steps),
                         ctypes.byref(sch), ctypes.byref(out), ptr(status), stream_ptr())
     _lib.check(rc, "nh_advance")
+
+
+def stream_workspace(B: int, N: int):
+    lib = require_cuda()
+    n = int(lib.nh_stream_workspace_bytes(B, N))
+    return torch().empty(n, dtype=torch().uint8, device="cuda")
+
+
+def stream_advance(members, h, hu, hw, time, n_steps, sch, status, workspace, flag_bits=None,
+                   p_out=None):
+    """Enqueue nh_stream_advance (tiled streaming kernels) on the current stream, in place."""
+    lib = require_cuda()
+    B, N = h.shape[0], h.shape[1]
+    out = _lib.Outputs(ptr(flag_bits), ptr(p_out), None)
+    rc = lib.nh_stream_advance(ptr(members), B, N, ptr(h), ptr(hu), ptr(hw), ptr(time),
+                               int(n_steps), ctypes.byref(sch), ctypes.byref(out), ptr(status),
+                               ptr(workspace), workspace.numel(), stream_ptr())
+    _lib.check(rc, "nh_stream_advance")

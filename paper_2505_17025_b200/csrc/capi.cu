@@ -5,6 +5,7 @@
 #include <mutex>
 #include <cstdlib>
 #include "step_kernel.cuh"
+#include "stream_kernels.cuh"
 
 extern "C" {
 int nh_launch_rhs(const nh_member*, int, int, const double*, const double*, const double*,
@@ -218,6 +219,93 @@ int nh_bottom_sample(const nh_member* members, int n_members, const double* x, i
                      const double* time, double* out, void* stream) {
   if (!members || n_members < 1 || n_points < 0) return NH_E_ARG;
   return nh_launch_bottom(members, n_members, x, n_points, time, out, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------- streaming path
+static int stream_tiles(int n) { return (n + NH_STREAM_OWN - 1) / NH_STREAM_OWN; }
+
+size_t nh_stream_workspace_bytes(int n_members, int n_elements) {
+  size_t BN = (size_t)n_members * n_elements, BT = (size_t)n_members * stream_tiles(n_elements);
+  size_t dbl = 6 * BN + 12 * BN + 12 * BN + 10 * BT;
+  return dbl * 8 + 2 * BN + 4 * (size_t)n_members + 1024;
+}
+
+int nh_stream_advance(const nh_member* members, int B, int N, double* h, double* hu, double* hw,
+                      double* time, int n_steps, const nh_scheme* scheme,
+                      const nh_outputs* outputs, nh_status* status, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  if (!members || !h || !hu || !hw || !time || !scheme || !status || !workspace) return NH_E_ARG;
+  if (B < 1 || N < 2 || n_steps < 0) return NH_E_ARG;
+  if (workspace_bytes < nh_stream_workspace_bytes(B, N)) return NH_E_ARG;
+  const nh_scheme& sc = *scheme;
+  if (sc.mode < NH_MODE_HYDROSTATIC || sc.mode > NH_MODE_ADAPTIVE) return NH_E_UNSUPPORTED;
+  if (sc.mode == NH_MODE_ADAPTIVE && (sc.criterion == NH_CRIT_W || sc.criterion == NH_CRIT_W_X))
+    return NH_E_UNSUPPORTED;   // member-wide any(hw) fallback lives in the resident kernel
+  if (sc.mode != NH_MODE_HYDROSTATIC && (sc.c12 != -0.5 || sc.c22 != 0.0)) return NH_E_UNSUPPORTED;
+  const int T = stream_tiles(N);
+  if ((T + 31) / 32 > NH_STREAM_MAXCPL) return NH_E_UNSUPPORTED;
+  if (n_steps == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t BN = (size_t)B * N, BT = (size_t)B * T;
+  char* w = (char*)workspace;
+  double* alt = (double*)w;             w += 6 * BN * 8;
+  double* scratch = (double*)w;         w += 12 * BN * 8;
+  double* pend[2] = {(double*)w, (double*)w + 6 * BN};  w += 12 * BN * 8;
+  double* tagg = (double*)w;            w += 8 * BT * 8;
+  double* tio = (double*)w;             w += 2 * BT * 8;
+  uint8_t* flags[2] = {(uint8_t*)w, (uint8_t*)w + BN};  w += 2 * BN;
+  int* counter = (int*)(((uintptr_t)w + 15) & ~(uintptr_t)15);
+  if (cudaMemsetAsync(counter, 0, 4 * (size_t)B, s) != cudaSuccess) return NH_E_CUDA;
+  double* A[3] = {h, hu, hw};
+  double* Bb[3] = {alt, alt + 2 * BN, alt + 4 * BN};
+  StreamArgs a = {};
+  a.members = members; a.time = time; a.status = status; a.step_counter = counter;
+  a.scratch = scratch; a.tile_agg = tagg; a.tile_io = tio;
+  a.flag_bits = outputs ? outputs->flag_bits : nullptr;
+  a.sch = sc; a.B = B; a.N = N; a.tiles = T; a.finalize = 0;
+  const dim3 gp(B * T), bp(NH_STREAM_THREADS), gx((B + 7) / 8), bx(256);
+  void* kp = nh_stream_kernel(0);
+  void* kx = nh_stream_kernel(1);
+  void* kc = nh_stream_kernel(2);
+  void* ks = nh_stream_kernel(3);
+  const bool corr = sc.mode != NH_MODE_HYDROSTATIC;
+  int cur = 0;   // 0: state in A, 1: state in Bb
+  for (int k = 0; k < n_steps; ++k) {
+    double** in = cur ? Bb : A;
+    double** out = cur ? A : Bb;
+    a.h_in = in[0]; a.hu_in = in[1]; a.hw_in = in[2];
+    a.h_out = out[0]; a.hu_out = out[1]; a.hw_out = out[2];
+    a.pend = (corr && k > 0) ? pend[(k - 1) & 1] : nullptr;
+    a.flags_prev = flags[(k - 1) & 1];
+    a.pend_out = pend[k & 1];
+    a.flags_cur = flags[k & 1];
+    void* args[1] = {&a};
+    if (cudaLaunchKernel(kp, gp, bp, args, 0, s) != cudaSuccess) return NH_E_CUDA;
+    if (corr && cudaLaunchKernel(ks, gp, bp, args, 0, s) != cudaSuccess) return NH_E_CUDA;
+    if (cudaLaunchKernel(kx, gx, bx, args, 0, s) != cudaSuccess) return NH_E_CUDA;
+    if (corr && cudaLaunchKernel(kc, gp, bp, args, 0, s) != cudaSuccess) return NH_E_CUDA;
+    cur ^= 1;
+  }
+  double** fin = cur ? Bb : A;
+  if (corr) {   // apply the last pending vertical-momentum update in place
+    a.h_in = fin[0]; a.hu_in = fin[1]; a.hw_in = fin[2];
+    a.pend = pend[(n_steps - 1) & 1];
+    a.flags_prev = flags[(n_steps - 1) & 1];
+    a.finalize = 1;
+    void* args[1] = {&a};
+    if (cudaLaunchKernel(kp, gp, bp, args, 0, s) != cudaSuccess) return NH_E_CUDA;
+  }
+  if (cur) {
+    for (int f = 0; f < 3; ++f)
+      if (cudaMemcpyAsync(A[f], Bb[f], 2 * BN * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return NH_E_CUDA;
+  }
+  if (outputs && outputs->p_nh && corr) {   // pressure of the last step, 0 off the ranges
+    // gather p from the pending record of the last step where its flag is set
+    const int last = (n_steps - 1) & 1;
+    if (nh_launch_gather_p(pend[last], flags[last], outputs->p_nh, BN, s)) return NH_E_CUDA;
+  }
+  return 0;
 }
 
 // diagnostics: device buffer [grid][NH_NPHASE] for NH_PROFILE_PHASES builds

@@ -1,0 +1,565 @@
+// Streaming (HBM round-trip) time step for large ensembles.
+//
+// One element per thread, 256-thread CTAs over tiles of OWN = 248 elements
+// plus a halo of H = 4 on each side, all CTAs independent (no clusters), so
+// the SMs run many CTAs at full occupancy and the step is bounded by HBM
+// traffic and the fp64 pipe rather than by barrier latency.  Per step:
+//
+//   K_P  (tile)   load the tile + halo (coalesced double2 per field), finish
+//                 the previous step's correction in registers -- the
+//                 vertical-momentum update needs the solved pressure of the
+//                 neighbours, so it is fused into the NEXT step's load
+//                 ("corrector fused with the next predictor") -- then both
+//                 Heun stages (hydrostatic.py:192-209), the criterion with
+//                 +-1 enlargement (adaptivity.py:75-113), the per-element
+//                 condensation of flagged elements (corrector.py:100-349 ->
+//                 physics.cuh) and the tile's merged super-element.
+//   K_X  (member) one warp per member merges its tiles' super-elements and
+//                 hands every tile its boundary inputs (a_in, z_in).
+//   K_C  (tile)   tiles holding flagged elements only: warp/CTA merge trees
+//                 down to the elements, hu replacement and pressure p.
+//
+// The three launches of a step and the ping-pong of buffers are captured in
+// a CUDA graph by the host (stream.py).  A final K_P in "finalize" mode
+// applies the last pending hw update in place.
+#include <cooperative_groups.h>
+#include "bathy.cuh"
+#include "physics.cuh"
+#include "stream_kernels.cuh"
+#include "tree.cuh"
+
+namespace {
+
+constexpr int TPB = NH_STREAM_THREADS;     // 256
+constexpr int H = NH_STREAM_HALO;          // 4
+constexpr int OWN = TPB - 2 * H;           // 248
+constexpr int NW = TPB / 32;
+
+__device__ __forceinline__ double ederiv(const nh_member& m, double v0, double v1, int i) {
+  return RMUL(fma(v1, m.deriv_ref[2 * i + 1], RMUL(v0, m.deriv_ref[2 * i])), m.two_over_dx);
+}
+
+struct Q6 {
+  double h0, h1, q0, q1, w0, w1;
+};
+
+// one Heun stage for the thread's element: node sides from the registers,
+// left face from the left neighbour's node-1 side (exchanged through smem),
+// right face from the right neighbour's left face (exchanged through smem)
+template <int KIND>
+__device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q6& q,
+                                           const BottomTime& bt, double x0, double x1, int i,
+                                           int e, int N, double* sh, double* sf, double t6[6],
+                                           double& speed) {
+  Bottom6 b0 = bottom_eval<KIND, false>(m, bt, x0);
+  Bottom6 b1 = bottom_eval<KIND, false>(m, bt, x1);
+  Side n0 = make_side(q.h0, q.q0, q.w0, b0.d);
+  Side n1 = make_side(q.h1, q.q1, q.w1, b1.d);
+  sh[0 * TPB + i] = q.h1; sh[1 * TPB + i] = q.q1; sh[2 * TPB + i] = q.w1; sh[3 * TPB + i] = b1.d;
+  __syncthreads();
+  Side L;
+  if (e == 0) {
+    L = ghost_side(n0, m.bc_left);
+  } else {
+    int k = i > 0 ? i - 1 : 0;
+    L = make_side(sh[0 * TPB + k], sh[1 * TPB + k], sh[2 * TPB + k], sh[3 * TPB + k]);
+  }
+  double sp;
+  Face fl = face_flux(L, n0, g, sp);
+  speed = fmax(speed, sp);
+  sf[0 * TPB + i] = fl.F1; sf[1 * TPB + i] = fl.F2L; sf[2 * TPB + i] = fl.F3;
+  __syncthreads();
+  Face fr;
+  if (e == N - 1) {
+    fr = face_flux(n1, ghost_side(n1, m.bc_right), g, sp);
+    speed = fmax(speed, sp);
+  } else {
+    int k = i < TPB - 1 ? i + 1 : i;
+    fr.F1 = sf[0 * TPB + k]; fr.F2L = sf[1 * TPB + k]; fr.F3 = sf[2 * TPB + k]; fr.F2R = 0.0;
+  }
+  element_tendency(m, g, n0, n1, fl, fr, b0.d_x, b1.d_x, t6);
+}
+
+__device__ __forceinline__ void store_super(double* dst, const Super& s) {
+  dst[0] = s.ga; dst[1] = s.aa; dst[2] = s.ba; dst[3] = s.gz; dst[4] = s.az; dst[5] = s.bz;
+}
+__device__ __forceinline__ Super load_super(const double* s) {
+  return Super{s[0], s[1], s[2], s[3], s[4], s[5]};
+}
+
+// CTA-level reduction of per-element super-elements (1 per thread) into the
+// tile aggregate.  Nodes are stored so that tile_down() can unwind them.
+__device__ __forceinline__ Super tile_up(Super agg, bool tflag, double* wnode, double* wagg,
+                                         double* bnode, int* wflag, int lane, int warp) {
+  const bool wany = __any_sync(0xffffffffu, tflag);
+  double* wn = wnode + warp * 31 * 6;
+  if (wany) {
+    agg = warp_up(agg, wn, lane, 5);
+  } else {
+    unsigned nonid = __ballot_sync(0xffffffffu, !is_identity(agg));
+    int first = nonid ? __ffs(nonid) - 1 : 0;
+    agg = shfl_super(agg, first);
+    if (!nonid) agg = super_identity();
+  }
+  if (lane == 0) {
+    store_super(wagg + warp * 6, agg);
+    wflag[warp] = wany ? 1 : 0;
+  }
+  __syncthreads();
+  Super v = super_identity();
+  if (warp == 0) {
+    if (lane < NW) v = load_super(wagg + lane * 6);
+    v = warp_up(v, bnode, lane, 3);
+  }
+  return v;   // valid in thread 0
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------- K_P
+struct KpSmem {
+  double sh[4 * TPB];
+  double sf[3 * TPB];
+  double wnode[NW * 31 * 6];
+  double wagg[NW * 6];
+  double bnode[31 * 6];
+  double cfl;
+  int wflag[NW];
+  uint8_t rf[TPB];
+};
+
+template <int KIND>
+__device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
+                                        const LdgConst& lk, KpSmem& ks) {
+  double* sh = ks.sh;
+  double* sf = ks.sf;
+  uint8_t* rf = ks.rf;
+  double* wnode = ks.wnode;
+  double* wagg = ks.wagg;
+  double* bnode = ks.bnode;
+  int* wflag = ks.wflag;
+  double& cfl_sh = ks.cfl;
+
+  const int N = a.N, T = a.tiles;
+  const int b = blockIdx.x / T, tile = blockIdx.x % T;
+  const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  const int e = tile * OWN - H + i;
+  const bool valid = e >= 0 && e < N;
+  const bool own = valid && i >= H && i < H + OWN;
+  const size_t o = ((size_t)b * N + (valid ? e : 0)) * 2;
+  const nh_scheme& sch = a.sch;
+  const double g = sch.g;
+  nh_status* st = a.status + b;
+  const int step = a.step_counter ? a.step_counter[b] : 0;
+  if (i == 0) cfl_sh = 0.0;
+
+  // ---------------- load (coalesced double2 per field) ----------------
+  Q6 q{1.0, 1.0, 0.0, 0.0, 0.0, 0.0};
+  if (valid) {
+    double2 vh = *reinterpret_cast<const double2*>(a.h_in + o);
+    double2 vq = *reinterpret_cast<const double2*>(a.hu_in + o);
+    double2 vw = *reinterpret_cast<const double2*>(a.hw_in + o);
+    q = Q6{vh.x, vh.y, vq.x, vq.y, vw.x, vw.y};
+  }
+
+  // ---------------- pending correction of the previous step ----------------
+  // hw += dt/rho (6/quad p + d_x/quad (h p)_x + phi) on flagged elements
+  // (corrector.py:441-482); (h p)_x lifts use the neighbours' (h p) traces.
+  if (a.pend) {
+    const bool f = valid && a.flags_prev[(size_t)b * N + e];
+    double p0 = 0.0, p1 = 0.0, phi0 = 0.0, phi1 = 0.0, dx0 = 0.0, dx1 = 0.0;
+    if (f) {
+      const double* pv = a.pend + ((size_t)b * N + e) * 6;
+      p0 = pv[0]; p1 = pv[1]; phi0 = pv[2]; phi1 = pv[3]; dx0 = pv[4]; dx1 = pv[5];
+    }
+    double hp0 = q.h0 * p0, hp1 = q.h1 * p1;
+    sh[0 * TPB + i] = hp0;
+    sh[1 * TPB + i] = hp1;
+    __syncthreads();
+    if (f) {
+      auto hp_of = [&](int ee, int node, int slot) -> double {
+        if (slot >= 0 && slot < TPB) return sh[node * TPB + slot];
+        // neighbour outside the CTA's slots (never needed for own elements)
+        if (!a.flags_prev[(size_t)b * N + ee]) return 0.0;
+        size_t oo = ((size_t)b * N + ee) * 2 + node;
+        return a.h_in[oo] * a.pend[((size_t)b * N + ee) * 6 + node];
+      };
+      double hx0 = ederiv(m, hp0, hp1, 0), hx1 = ederiv(m, hp0, hp1, 1);
+      if (e < N - 1) {
+        double hr = hp_of(e + 1, 0, i + 1);
+        double avg = 0.5 * (hp1 + hr);
+        hx0 += (avg - hp1) * m.lift_right[0];
+        hx1 += (avg - hp1) * m.lift_right[1];
+      }
+      if (e > 0) {
+        double hl = hp_of(e - 1, 1, i - 1);
+        double avg = 0.5 * (hl + hp0);
+        hx0 -= (avg - hp0) * m.lift_left[0];
+        hx1 -= (avg - hp0) * m.lift_left[1];
+      }
+      double qd0 = 4.0 + dx0 * dx0, qd1 = 4.0 + dx1 * dx1;
+      double bp0 = nh_div(6.0, qd0) * p0 + nh_div(dx0, qd0) * hx0 + phi0;
+      double bp1 = nh_div(6.0, qd1) * p1 + nh_div(dx1, qd1) * hx1 + phi1;
+      q.w0 += lk.cdt * bp0;
+      q.w1 += lk.cdt * bp1;
+    }
+    __syncthreads();
+  }
+  if (a.finalize) {
+    if (own) {
+      double2 vw{q.w0, q.w1};
+      *reinterpret_cast<double2*>(const_cast<double*>(a.hw_in) + o) = vw;
+    }
+    return;
+  }
+
+  const double t = a.time[b], dt = m.dt, t1 = t + dt;
+  const double ed = (double)e;
+  const double x0 = sample_xd(m, ed, 0), x1 = sample_xd(m, ed, 1);
+  double speed = 0.0;
+
+  // ---------------- Heun stage 1 at t ----------------
+  if (own && (q.h0 <= 0.0 || q.h1 <= 0.0)) nh_report(st, step, NH_ERR_POSITIVITY_ENTRY, e);
+  BottomTime bt0 = bottom_time_k<KIND>(m, t);
+  double k1[6];
+  stage_tend<KIND>(m, g, q, bt0, x0, x1, i, e, N, sh, sf, k1, speed);
+  Q6 qs{RADD(q.h0, RMUL(dt, k1[0])), RADD(q.h1, RMUL(dt, k1[1])),
+        RADD(q.q0, RMUL(dt, k1[2])), RADD(q.q1, RMUL(dt, k1[3])),
+        RADD(q.w0, RMUL(dt, k1[4])), RADD(q.w1, RMUL(dt, k1[5]))};
+  if (own && !(qs.h0 > 0.0 && qs.h1 > 0.0)) nh_report(st, step, NH_ERR_POSITIVITY_STAGE1, -1);
+  __syncthreads();   // every read of sh / sf of stage 1 is done
+
+  // ---------------- Heun stage 2 at t + dt ----------------
+  BottomTime bt1 = bottom_time_k<KIND>(m, t1);
+  double k2[6];
+  {
+    double dummy = 0.0;
+    stage_tend<KIND>(m, g, qs, bt1, x0, x1, i, e, N, sh, sf, k2, dummy);
+  }
+  Q6 qp{RADD(q.h0, RMUL(dt, RMUL(0.5, RADD(k1[0], k2[0])))),
+        RADD(q.h1, RMUL(dt, RMUL(0.5, RADD(k1[1], k2[1])))),
+        RADD(q.q0, RMUL(dt, RMUL(0.5, RADD(k1[2], k2[2])))),
+        RADD(q.q1, RMUL(dt, RMUL(0.5, RADD(k1[3], k2[3])))),
+        RADD(q.w0, RMUL(dt, RMUL(0.5, RADD(k1[4], k2[4])))),
+        RADD(q.w1, RMUL(dt, RMUL(0.5, RADD(k1[5], k2[5]))))};
+  if (own && !(qp.h0 > 0.0 && qp.h1 > 0.0)) nh_report(st, step, NH_ERR_POSITIVITY_STAGE2, -1);
+  if (own) {
+    *reinterpret_cast<double2*>(a.h_out + o) = double2{qp.h0, qp.h1};
+    *reinterpret_cast<double2*>(a.hu_out + o) = double2{qp.q0, qp.q1};
+    *reinterpret_cast<double2*>(a.hw_out + o) = double2{qp.w0, qp.w1};
+  }
+  if (sch.record_cfl) {   // all lanes take part in the shuffles (halo lanes contribute 0)
+    double c = own ? speed * dt / m.dx : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) c = fmax(c, __shfl_down_sync(0xffffffffu, c, off));
+    if (lane == 0) atomicMax((unsigned long long*)&cfl_sh, (unsigned long long)__double_as_longlong(c));
+  }
+  if (sch.mode == NH_MODE_HYDROSTATIC) {
+    __syncthreads();
+    if (i == 0 && cfl_sh > 0.0)
+      atomicMax((unsigned long long*)&st->cfl_max, (unsigned long long)__double_as_longlong(cfl_sh));
+    return;
+  }
+
+  // ---------------- criterion on the predictor (t + dt) ----------------
+  uint8_t raw = 0;
+  if (valid) {
+    if (sch.mode == NH_MODE_GLOBAL) {
+      raw = 1;
+    } else {
+      double v0, v1;
+      switch (sch.criterion) {
+        case NH_CRIT_ETA_OVER_D: {
+          double d0 = bottom_eval<KIND, false>(m, bt1, x0).d;
+          double d1 = bottom_eval<KIND, false>(m, bt1, x1).d;
+          v0 = fabs(RDIV(RSUB(qp.h0, d0), d0)); v1 = fabs(RDIV(RSUB(qp.h1, d1), d1));
+          break;
+        }
+        case NH_CRIT_ETA_X: {
+          double d0 = bottom_eval<KIND, false>(m, bt1, x0).d;
+          double d1 = bottom_eval<KIND, false>(m, bt1, x1).d;
+          v0 = fabs(ederiv(m, RSUB(qp.h0, d0), RSUB(qp.h1, d1), 0));
+          v1 = fabs(ederiv(m, RSUB(qp.h0, d0), RSUB(qp.h1, d1), 1));
+          break;
+        }
+        case NH_CRIT_U:
+          v0 = fabs(RDIV(qp.q0, qp.h0)); v1 = fabs(RDIV(qp.q1, qp.h1));
+          break;
+        case NH_CRIT_U_X: {
+          double u0 = RDIV(qp.q0, qp.h0), u1 = RDIV(qp.q1, qp.h1);
+          v0 = fabs(ederiv(m, u0, u1, 0)); v1 = fabs(ederiv(m, u0, u1, 1));
+          break;
+        }
+        case NH_CRIT_W:
+          v0 = fabs(RDIV(qp.w0, qp.h0)); v1 = fabs(RDIV(qp.w1, qp.h1));
+          break;
+        default: {
+          double w0 = RDIV(qp.w0, qp.h0), w1 = RDIV(qp.w1, qp.h1);
+          v0 = fabs(ederiv(m, w0, w1, 0)); v1 = fabs(ederiv(m, w0, w1, 1));
+          break;
+        }
+      }
+      raw = fmax(v0, v1) > sch.k_nh ? 1 : 0;
+    }
+  }
+  rf[i] = raw;
+  __syncthreads();
+  const bool enl = sch.mode == NH_MODE_ADAPTIVE && sch.enlarge;
+  auto eff = [&](int s) -> bool {
+    int ee = tile * OWN - H + s;
+    if (ee < 0 || ee >= N || s < 0 || s >= TPB) return false;
+    bool f = rf[s] != 0;
+    if (enl) {
+      if (ee > 0 && s > 0) f = f || rf[s - 1];
+      if (ee < N - 1 && s + 1 < TPB) f = f || rf[s + 1];
+    }
+    return f;
+  };
+  const bool flag = own && eff(i);
+  if (own) a.flags_cur[(size_t)b * N + e] = flag ? 1 : 0;
+  if (flag && a.flag_bits) {
+    uint32_t* fb = a.flag_bits + ((size_t)step * a.B + b) * ((N + 31) / 32);
+    atomicOr(fb + (e >> 5), 1u << (e & 31));
+  }
+
+  // ---------------- per-tile flagged count; unflagged tiles aggregate to a gap ----------------
+  {
+    int nf = __syncthreads_count(flag);
+    if (i == H) {   // first own slot
+      double* ta = a.tile_agg + ((size_t)b * T + tile) * 8;
+      ta[6] = (double)nf;
+      if (nf == 0) store_super(ta, super_gap(qp.q0));
+      if (nf) atomicAdd((unsigned long long*)&st->flagged, (unsigned long long)nf);
+    }
+    // right-end ghost outer trace (corrector.py:400-402)
+    if (e == N - 1 && own) {
+      double qq = qp.q1;
+      a.tile_agg[((size_t)b * T + tile) * 8 + 7] = (m.bc_right == NH_BC_WALL) ? -qq : qq;
+    }
+  }
+  if (i == 0 && cfl_sh > 0.0)
+    atomicMax((unsigned long long*)&st->cfl_max, (unsigned long long)__double_as_longlong(cfl_sh));
+}
+
+// ---------------------------------------------------------------------- K_S
+// Tiles holding flagged elements: LDG coefficients at t+dt and the per-element
+// condensation (corrector.py:100-349 -> physics.cuh), stored for K_C, and the
+// tile's merged super-element for K_X.
+template <int KIND>
+__device__ __forceinline__ void ks_body(const StreamArgs& a, const nh_member& m,
+                                        const LdgConst& lk, KpSmem& ks) {
+  const int N = a.N, T = a.tiles;
+  const int b = blockIdx.x / T, tile = blockIdx.x % T;
+  const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  const int e = tile * OWN - H + i;
+  const bool valid = e >= 0 && e < N;
+  const bool own = valid && i >= H && i < H + OWN;
+  const size_t o = ((size_t)b * N + (valid ? e : 0)) * 2;
+  const size_t fe = (size_t)b * N + (valid ? e : 0);
+  const bool flag = own && a.flags_cur[fe];
+  nh_status* st = a.status + b;
+  const int step = a.step_counter ? a.step_counter[b] : 0;
+  Super S = super_identity();
+  if (own) S = super_gap(a.hu_out[o]);
+  if (flag) {
+    const double t1 = a.time[b] + m.dt;
+    const BottomTime bt1 = bottom_time_k<KIND>(m, t1);
+    const double ed = (double)e;
+    const double x0 = sample_xd(m, ed, 0), x1 = sample_xd(m, ed, 1);
+    double2 vh = *reinterpret_cast<const double2*>(a.h_out + o);
+    double2 vq = *reinterpret_cast<const double2*>(a.hu_out + o);
+    double2 vw = *reinterpret_cast<const double2*>(a.hw_out + o);
+    const bool range_end = (e == N - 1) || !a.flags_cur[fe + 1];
+    Bottom6 b0 = bottom_eval<KIND, true>(m, bt1, x0);
+    Bottom6 b1 = bottom_eval<KIND, true>(m, bt1, x1);
+    Chan ch0{b0.d, b0.d_x, b0.d_t, b0.d_tt, b0.d_xt, b0.d_xx};
+    Chan ch1{b1.d, b1.d_x, b1.d_t, b1.d_tt, b1.d_xt, b1.d_xx};
+    double exa = ederiv(m, vh.x - b0.d, vh.y - b1.d, 0);
+    double exb = ederiv(m, vh.x - b0.d, vh.y - b1.d, 1);
+    NodeCoef c0 = ldg_coefficients(vh.x, vq.x, vw.x, ederiv(m, vh.x, vh.y, 0), exa, ch0, lk);
+    NodeCoef c1 = ldg_coefficients(vh.y, vq.y, vw.y, ederiv(m, vh.x, vh.y, 1), exb, ch1, lk);
+    double R[6];
+    if (!local_condense(m, c0, c1, lk.rho, lk.inv_rho, a.sch.c11, range_end, S, R))
+      nh_report(st, step, NH_ERR_SOLVE_PIVOT, e);
+    double* sc = a.scratch + fe * 12;
+    store_super(sc, S);
+    sc[6] = R[0]; sc[7] = R[1]; sc[8] = R[2]; sc[9] = R[3]; sc[10] = R[4]; sc[11] = R[5];
+    double* pn = a.pend_out + fe * 6;
+    pn[2] = c0.phi; pn[3] = c1.phi; pn[4] = b0.d_x; pn[5] = b1.d_x;
+  }
+  Super v = tile_up(S, flag, ks.wnode, ks.wagg, ks.bnode, ks.wflag, lane, warp);
+  if (i == 0) store_super(a.tile_agg + ((size_t)b * T + tile) * 8, v);
+}
+
+__global__ void __launch_bounds__(TPB) nh_stream_ks(StreamArgs a) {
+  __shared__ nh_member msh;
+  __shared__ LdgConst ksh;
+  __shared__ KpSmem ks;
+  const int b = blockIdx.x / a.tiles;
+  if (!(a.tile_agg[(size_t)blockIdx.x * 8 + 6] > 0.0)) return;   // no flagged element
+  if (threadIdx.x < (int)(sizeof(nh_member) / 8))
+    reinterpret_cast<unsigned long long*>(&msh)[threadIdx.x] =
+        reinterpret_cast<const unsigned long long*>(a.members + b)[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) ksh = make_ldg_const(msh.dt, a.sch.g, a.sch.rho);
+  __syncthreads();
+  switch (msh.bottom_kind) {
+    case NH_BOTTOM_FLAT: ks_body<NH_BOTTOM_FLAT>(a, msh, ksh, ks); break;
+    case NH_BOTTOM_PLATE: ks_body<NH_BOTTOM_PLATE>(a, msh, ksh, ks); break;
+    case NH_BOTTOM_QUARTIC_SLIDE: ks_body<NH_BOTTOM_QUARTIC_SLIDE>(a, msh, ksh, ks); break;
+    case NH_BOTTOM_SMOOTH_BOX: ks_body<NH_BOTTOM_SMOOTH_BOX>(a, msh, ksh, ks); break;
+    default: ks_body<NH_BOTTOM_SLOPE_SLIDE>(a, msh, ksh, ks); break;
+  }
+}
+
+__global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(StreamArgs a) {
+  __shared__ nh_member msh;
+  __shared__ LdgConst ksh;
+  __shared__ KpSmem ks;
+  const int b = blockIdx.x / a.tiles;
+  // cooperative copy of the 312-byte member record (one 8-byte word per thread)
+  if (threadIdx.x < (int)(sizeof(nh_member) / 8))
+    reinterpret_cast<unsigned long long*>(&msh)[threadIdx.x] =
+        reinterpret_cast<const unsigned long long*>(a.members + b)[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) ksh = make_ldg_const(msh.dt, a.sch.g, a.sch.rho);
+  __syncthreads();
+  switch (msh.bottom_kind) {
+    case NH_BOTTOM_FLAT: kp_body<NH_BOTTOM_FLAT>(a, msh, ksh, ks); break;
+    case NH_BOTTOM_PLATE: kp_body<NH_BOTTOM_PLATE>(a, msh, ksh, ks); break;
+    case NH_BOTTOM_QUARTIC_SLIDE: kp_body<NH_BOTTOM_QUARTIC_SLIDE>(a, msh, ksh, ks); break;
+    case NH_BOTTOM_SMOOTH_BOX: kp_body<NH_BOTTOM_SMOOTH_BOX>(a, msh, ksh, ks); break;
+    default: kp_body<NH_BOTTOM_SLOPE_SLIDE>(a, msh, ksh, ks); break;
+  }
+}
+
+// ---------------------------------------------------------------------- K_X
+// One warp per member: chain of its T tile aggregates (lane l folds tiles
+// [l*cpl, (l+1)*cpl)), merge tree across lanes, back-substitution, then each
+// tile's (a_in, z_in).  Also advances the member's time and step counter.
+__global__ void __launch_bounds__(256) nh_stream_kx(StreamArgs a) {
+  __shared__ double nodes[8][31 * 6];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * 8 + warp;
+  if (b >= a.B) return;
+  const int T = a.tiles;
+  const int cpl = (T + 31) / 32;
+  const double* ta = a.tile_agg + (size_t)b * T * 8;
+  bool any = false;
+  for (int k = lane; k < T; k += 32) any |= ta[k * 8 + 6] > 0.0;
+  any = __any_sync(0xffffffffu, any);
+  double* io = a.tile_io + (size_t)b * T * 2;
+  if (any) {
+    Super agg = super_identity();
+    int k0 = lane * cpl, k1 = min(k0 + cpl, T);
+    for (int k = k0; k < k1; ++k) agg = merge2(agg, load_super(ta + k * 8));
+    warp_up(agg, nodes[warp], lane, 5);
+    double a_in = 0.0, z_in = ta[(T - 1) * 8 + 7];
+    warp_down(a_in, z_in, nodes[warp], lane, 5);
+    // unwind this lane's tiles (Riccati sweep, exact elimination)
+    double s = a_in, tt = 0.0;
+    double sv[NH_STREAM_MAXCPL], tv[NH_STREAM_MAXCPL], mv[NH_STREAM_MAXCPL], nv[NH_STREAM_MAXCPL];
+    for (int k = k0; k < k1; ++k) {
+      sv[k - k0] = s; tv[k - k0] = tt;
+      riccati_step(load_super(ta + k * 8), s, tt, mv[k - k0], nv[k - k0]);
+    }
+    double z = z_in;
+    for (int k = k1 - 1; k >= k0; --k) {
+      io[k * 2 + 1] = z;
+      z = fma(nv[k - k0], z, mv[k - k0]);
+      io[k * 2 + 0] = fma(tv[k - k0], z, sv[k - k0]);
+    }
+  }
+  if (lane == 0) {
+    a.time[b] = a.time[b] + a.members[b].dt;
+    if (a.step_counter) a.step_counter[b] += 1;
+  }
+}
+
+// ---------------------------------------------------------------------- K_C
+__global__ void __launch_bounds__(TPB) nh_stream_kc(StreamArgs a) {
+  __shared__ double wnode[NW * 31 * 6];
+  __shared__ double wagg[NW * 6];
+  __shared__ double bnode[31 * 6];
+  __shared__ double wio[NW * 2];
+  __shared__ int wflag[NW];
+  const int N = a.N, T = a.tiles;
+  const int b = blockIdx.x / T, tile = blockIdx.x % T;
+  const double* ta = a.tile_agg + ((size_t)b * T + tile) * 8;
+  if (!(ta[6] > 0.0)) return;                         // no flagged element in this tile
+  const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  const int e = tile * OWN - H + i;
+  const bool valid = e >= 0 && e < N;
+  const bool own = valid && i >= H && i < H + OWN;
+  const size_t o = ((size_t)b * N + (valid ? e : 0)) * 2;
+  const bool flag = own && a.flags_cur[(size_t)b * N + e];
+  Super S = super_identity();
+  double R[6] = {0, 0, 0, 0, 0, 0};
+  if (flag) {
+    const double* sc = a.scratch + ((size_t)b * N + e) * 12;
+    S = load_super(sc);
+    R[0] = sc[6]; R[1] = sc[7]; R[2] = sc[8]; R[3] = sc[9]; R[4] = sc[10]; R[5] = sc[11];
+  } else if (own) {
+    S = super_gap(a.hu_out[o]);
+  }
+  // up: the same trees K_P built (recomputed from the stored super-elements)
+  const bool wany = __any_sync(0xffffffffu, flag);
+  double* wn = wnode + warp * 31 * 6;
+  Super agg = S;
+  if (wany) {
+    agg = warp_up(agg, wn, lane, 5);
+  } else {
+    unsigned nonid = __ballot_sync(0xffffffffu, !is_identity(agg));
+    int first = nonid ? __ffs(nonid) - 1 : 0;
+    agg = shfl_super(agg, first);
+    if (!nonid) agg = super_identity();
+  }
+  if (lane == 0) store_super(wagg + warp * 6, agg);
+  __syncthreads();
+  if (warp == 0) {
+    Super v = lane < NW ? load_super(wagg + lane * 6) : super_identity();
+    warp_up(v, bnode, lane, 3);
+    const double* io = a.tile_io + ((size_t)b * T + tile) * 2;
+    double ai = lane == 0 ? io[0] : 0.0, zi = lane == 0 ? io[1] : 0.0;
+    warp_down(ai, zi, bnode, lane, 3);
+    if (lane < NW) { wio[lane * 2] = ai; wio[lane * 2 + 1] = zi; }
+  }
+  __syncthreads();
+  if (!wany) return;
+  double a_in = wio[warp * 2], z_in = wio[warp * 2 + 1];
+  warp_down(a_in, z_in, wn, lane, 5);
+  if (!flag) return;
+  double P0, P1, Q0, Q1;
+  reconstruct(S, R, a_in, z_in, a.sch.c11, P0, P1, Q0, Q1);
+  if (!isfinite(P0 + P1 + Q0 + Q1)) {
+    int step = a.step_counter ? a.step_counter[b] - 1 : 0;
+    nh_report(a.status + b, step, NH_ERR_SOLVE_NONFINITE, e);
+  }
+  *reinterpret_cast<double2*>(a.hu_out + o) = double2{Q0, Q1};
+  double* pn = a.pend_out + ((size_t)b * N + e) * 6;
+  pn[0] = a.sch.rho * P0;
+  pn[1] = a.sch.rho * P1;
+}
+
+__global__ void nh_gather_p_kernel(const double* pend, const uint8_t* flags, double* p, size_t n) {
+  size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  bool f = flags[k];
+  p[2 * k] = f ? pend[6 * k] : 0.0;
+  p[2 * k + 1] = f ? pend[6 * k + 1] : 0.0;
+}
+
+int nh_launch_gather_p(const double* pend, const uint8_t* flags, double* p, size_t n,
+                       cudaStream_t s) {
+  nh_gather_p_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pend, flags, p, n);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+void* nh_stream_kernel(int which) {
+  switch (which) {
+    case 0: return (void*)nh_stream_kp;
+    case 1: return (void*)nh_stream_kx;
+    case 3: return (void*)nh_stream_ks;
+    default: return (void*)nh_stream_kc;
+  }
+}

@@ -1,0 +1,40 @@
+// Streaming step kernels: shared declarations (stream_kernels.cu, capi.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include "../../include/nhswe_b200.h"
+
+#define NH_STREAM_THREADS 256
+#define NH_STREAM_HALO 4
+#define NH_STREAM_OWN (NH_STREAM_THREADS - 2 * NH_STREAM_HALO)
+#define NH_STREAM_MAXCPL 8
+#ifndef NH_STREAM_MIN_BLOCKS
+#define NH_STREAM_MIN_BLOCKS 4
+#endif   // tiles per lane in K_X: members up to 32*8*248 elements
+
+struct StreamArgs {
+  const nh_member* members;
+  const double* h_in;
+  const double* hu_in;
+  const double* hw_in;
+  double* h_out;
+  double* hu_out;
+  double* hw_out;
+  const uint8_t* flags_prev;   // flags of the step whose correction is pending (or unused)
+  uint8_t* flags_cur;
+  const double* pend;          // [B][N][6] p0 p1 phi0 phi1 dx0 dx1 of the pending step, or NULL
+  double* pend_out;            // same, for this step
+  double* scratch;             // [B][N][12] super-element + reconstruction rows
+  double* tile_agg;            // [B][T][8] aggregate (6), flagged count, right ghost
+  double* tile_io;             // [B][T][2] (a_in, z_in)
+  double* time;                // [B]
+  int* step_counter;           // [B] steps done in this call
+  nh_status* status;
+  uint32_t* flag_bits;         // optional [n_steps][B][nwords]
+  nh_scheme sch;
+  int B, N, tiles, finalize;
+};
+
+void* nh_stream_kernel(int which);
+int nh_launch_gather_p(const double* pend, const uint8_t* flags, double* p, size_t n,
+                       cudaStream_t s);

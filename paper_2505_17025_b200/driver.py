@@ -82,18 +82,36 @@ class Ensemble:
     def reset_status(self):
         self.status = D.new_status(self.B)
 
+    def choose_path(self, mode: str, criterion: Criterion | None) -> str:
+        """Streaming tiles for ensembles that fill the GPU, the SMEM-resident
+        cluster kernel for small runs (lower per-step latency) and for the
+        w / w_x criteria (their first-step fallback needs a member-wide
+        reduction of the step's input, adaptivity.py:153)."""
+        if mode == "adaptive" and criterion is not None and criterion.kind in ("w", "w_x"):
+            return "resident"
+        tiles = self.B * ((self.N + 247) // 248)
+        return "stream" if tiles >= 2 * 148 else "resident"
+
     def advance(self, n_steps: int, mode: str = "adaptive", criterion: Criterion | None = None,
                 flux: FluxCoefficients = FluxCoefficients(), g: float = 9.81,
-                rho: float = RHO_WATER, flag_bits=None, p_out=None):
-        """Enqueue n_steps fused steps on the current stream (asynchronous)."""
+                rho: float = RHO_WATER, flag_bits=None, p_out=None, path: str = "auto"):
+        """Enqueue n_steps time steps on the current stream (asynchronous)."""
         if mode not in _MODES:
             raise ValueError(f"unknown mode {mode!r}")
         if mode == "adaptive" and criterion is None:
             raise ValueError("adaptive mode requires a criterion")
         c = criterion if criterion is not None else Criterion("eta_over_d")
         sch = D.scheme(_MODES[mode], c.kind, c.k_nh, c.enlarge, flux, g, rho)
-        D.advance(self.members, self.h, self.hu, self.hw, self.time, n_steps, sch, self.status,
-                  flag_bits, p_out)
+        if path == "auto":
+            path = self.choose_path(mode, criterion)
+        if path == "stream":
+            if getattr(self, "_ws", None) is None:
+                self._ws = D.stream_workspace(self.B, self.N)
+            D.stream_advance(self.members, self.h, self.hu, self.hw, self.time, n_steps, sch,
+                             self.status, self._ws, flag_bits, p_out)
+        else:
+            D.advance(self.members, self.h, self.hu, self.hw, self.time, n_steps, sch,
+                      self.status, flag_bits, p_out)
 
     def check(self, t0=None):
         """Raise the reference exception for the first failed member, if any."""

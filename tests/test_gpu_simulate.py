@@ -79,8 +79,11 @@ def test_long_member_cluster_global():
     assert np.abs(st.hw.values - ow).max() <= 1e-10 * np.abs(ow).max()
 
 
-def test_ensemble_mixed_members():
-    """Config-4 style mixed ensemble (solitary + box uplift), per-member dt / dx."""
+@pytest.mark.parametrize("path", ["resident", "stream"])
+@pytest.mark.parametrize("mode,enlarge", [("adaptive", False), ("adaptive", True), ("global", False)])
+def test_ensemble_mixed_members(path, mode, enlarge):
+    """Config-4 style mixed ensemble (solitary + box uplift), per-member dt / dx,
+    through both step implementations (SMEM-resident clusters / streaming tiles)."""
     cfg = configs.Config4(n_members=6, n_elements=512, n_steps=120)
     recs = cfg.records()
     states = [cfg.host_state(i, oracle_depth) for i in range(cfg.n_members)]
@@ -88,22 +91,25 @@ def test_ensemble_mixed_members():
     Q = np.stack([s[1] for s in states])
     Wv = np.stack([s[2] for s in states])
     ens = P.Ensemble.from_host(recs, H, Q, Wv)
-    crit = P.Criterion("eta_over_d")
-    ens.advance(cfg.n_steps, "adaptive", crit)
+    crit = P.Criterion("eta_over_d", 1e-3, enlarge)
+    ens.advance(cfg.n_steps, mode, crit, path=path)
     st = ens.check()
     gh, gq, gw = (x.cpu().numpy() for x in (ens.h, ens.hu, ens.hw))
     for i in range(cfg.n_members):
         m = cfg.member(i)
         mem = oracle_member(m.grid, m.bathymetry, m.bcs, m.dt)
-        r = O.run(mem, H[i], Q[i], Wv[i], cfg.n_steps, mode="adaptive")
-        assert rel(gh[i] - m.bathymetry.h0, r.h - m.bathymetry.h0) <= 1e-9, i
-        assert rel(gq[i], r.hu) <= 1e-9, i
+        r = O.run(mem, H[i], Q[i], Wv[i], cfg.n_steps, mode=mode, enlarge=enlarge)
+        assert rel(gh[i] - m.bathymetry.h0, r.h - m.bathymetry.h0) <= 1e-9, (i, path)
+        assert rel(gq[i], r.hu) <= 1e-9, (i, path)
+        assert np.abs(gw[i] - r.hw).max() <= 1e-9 * max(np.abs(r.hw).max(), 1e-12), (i, path)
         assert abs(st["flagged"][i] / (cfg.n_steps * cfg.n_elements) - r.fraction_mean) < 1e-3
+        assert float(ens.time[i].item()) == r.t, (i, path)
 
 
+@pytest.mark.parametrize("path", ["resident", "stream"])
 @pytest.mark.parametrize("cfg_name,members,n_steps", [("config4", (0, 1, 2047, 4095), 200),
                                                       ("config5", (0, 65535), 40)])
-def test_sampled_ensemble_members_full_size(cfg_name, members, n_steps):
+def test_sampled_ensemble_members_full_size(cfg_name, members, n_steps, path):
     """Sampled members of the throughput configs at full N, stepped inside the
     batched ensemble path, against the oracle run of the same members."""
     cfg = configs.Config4() if cfg_name == "config4" else configs.Config5()
@@ -113,7 +119,7 @@ def test_sampled_ensemble_members_full_size(cfg_name, members, n_steps):
     H, Q, W = (np.stack([s[k] for s in states]) for k in range(3))
     ens = P.Ensemble.from_host(recs, H, Q, W)
     mode = "adaptive"
-    ens.advance(n_steps, mode, P.Criterion("eta_over_d"))
+    ens.advance(n_steps, mode, P.Criterion("eta_over_d"), path=path)
     st = ens.check()
     gh, gq, gw = (x.cpu().numpy() for x in (ens.h, ens.hu, ens.hw))
     for k, i in enumerate(idx):
