@@ -120,12 +120,17 @@ __device__ __forceinline__ Super tile_up(Super agg, bool tflag, double* wnode, d
 struct KpSmem {
   double sh[4 * TPB];
   double sf[3 * TPB];
+  double sk[6 * TPB];     // k1 of this thread's element
+  double sq[6 * TPB];     // step-start state of this thread's element
+  double cfl;
+  uint8_t rf[TPB];
+};
+
+struct KsSmem {
   double wnode[NW * 31 * 6];
   double wagg[NW * 6];
   double bnode[31 * 6];
-  double cfl;
   int wflag[NW];
-  uint8_t rf[TPB];
 };
 
 template <int KIND>
@@ -134,10 +139,6 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   double* sh = ks.sh;
   double* sf = ks.sf;
   uint8_t* rf = ks.rf;
-  double* wnode = ks.wnode;
-  double* wagg = ks.wagg;
-  double* bnode = ks.bnode;
-  int* wflag = ks.wflag;
   double& cfl_sh = ks.cfl;
 
   const int N = a.N, T = a.tiles;
@@ -220,12 +221,19 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
 
   // ---------------- Heun stage 1 at t ----------------
   if (own && (q.h0 <= 0.0 || q.h1 <= 0.0)) nh_report(st, step, NH_ERR_POSITIVITY_ENTRY, e);
-  BottomTime bt0 = bottom_time_k<KIND>(m, t);
-  double k1[6];
-  stage_tend<KIND>(m, g, q, bt0, x0, x1, i, e, N, sh, sf, k1, speed);
-  Q6 qs{RADD(q.h0, RMUL(dt, k1[0])), RADD(q.h1, RMUL(dt, k1[1])),
-        RADD(q.q0, RMUL(dt, k1[2])), RADD(q.q1, RMUL(dt, k1[3])),
-        RADD(q.w0, RMUL(dt, k1[4])), RADD(q.w1, RMUL(dt, k1[5]))};
+  ks.sq[0 * TPB + i] = q.h0; ks.sq[1 * TPB + i] = q.h1; ks.sq[2 * TPB + i] = q.q0;
+  ks.sq[3 * TPB + i] = q.q1; ks.sq[4 * TPB + i] = q.w0; ks.sq[5 * TPB + i] = q.w1;
+  Q6 qs;
+  {
+    BottomTime bt0 = bottom_time_k<KIND>(m, t);
+    double k1[6];
+    stage_tend<KIND>(m, g, q, bt0, x0, x1, i, e, N, sh, sf, k1, speed);
+#pragma unroll
+    for (int f = 0; f < 6; ++f) ks.sk[f * TPB + i] = k1[f];
+    qs = Q6{RADD(q.h0, RMUL(dt, k1[0])), RADD(q.h1, RMUL(dt, k1[1])),
+            RADD(q.q0, RMUL(dt, k1[2])), RADD(q.q1, RMUL(dt, k1[3])),
+            RADD(q.w0, RMUL(dt, k1[4])), RADD(q.w1, RMUL(dt, k1[5]))};
+  }
   if (own && !(qs.h0 > 0.0 && qs.h1 > 0.0)) nh_report(st, step, NH_ERR_POSITIVITY_STAGE1, -1);
   __syncthreads();   // every read of sh / sf of stage 1 is done
 
@@ -236,12 +244,11 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
     double dummy = 0.0;
     stage_tend<KIND>(m, g, qs, bt1, x0, x1, i, e, N, sh, sf, k2, dummy);
   }
-  Q6 qp{RADD(q.h0, RMUL(dt, RMUL(0.5, RADD(k1[0], k2[0])))),
-        RADD(q.h1, RMUL(dt, RMUL(0.5, RADD(k1[1], k2[1])))),
-        RADD(q.q0, RMUL(dt, RMUL(0.5, RADD(k1[2], k2[2])))),
-        RADD(q.q1, RMUL(dt, RMUL(0.5, RADD(k1[3], k2[3])))),
-        RADD(q.w0, RMUL(dt, RMUL(0.5, RADD(k1[4], k2[4])))),
-        RADD(q.w1, RMUL(dt, RMUL(0.5, RADD(k1[5], k2[5]))))};
+  double qv[6];
+#pragma unroll
+  for (int f = 0; f < 6; ++f)
+    qv[f] = RADD(ks.sq[f * TPB + i], RMUL(dt, RMUL(0.5, RADD(ks.sk[f * TPB + i], k2[f]))));
+  Q6 qp{qv[0], qv[1], qv[2], qv[3], qv[4], qv[5]};
   if (own && !(qp.h0 > 0.0 && qp.h1 > 0.0)) nh_report(st, step, NH_ERR_POSITIVITY_STAGE2, -1);
   if (own) {
     *reinterpret_cast<double2*>(a.h_out + o) = double2{qp.h0, qp.h1};
@@ -347,7 +354,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
 // tile's merged super-element for K_X.
 template <int KIND>
 __device__ __forceinline__ void ks_body(const StreamArgs& a, const nh_member& m,
-                                        const LdgConst& lk, KpSmem& ks) {
+                                        const LdgConst& lk, KsSmem& ks) {
   const int N = a.N, T = a.tiles;
   const int b = blockIdx.x / T, tile = blockIdx.x % T;
   const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
@@ -394,7 +401,7 @@ __device__ __forceinline__ void ks_body(const StreamArgs& a, const nh_member& m,
 __global__ void __launch_bounds__(TPB) nh_stream_ks(StreamArgs a) {
   __shared__ nh_member msh;
   __shared__ LdgConst ksh;
-  __shared__ KpSmem ks;
+  __shared__ KsSmem ks;
   const int b = blockIdx.x / a.tiles;
   if (!(a.tile_agg[(size_t)blockIdx.x * 8 + 6] > 0.0)) return;   // no flagged element
   if (threadIdx.x < (int)(sizeof(nh_member) / 8))
