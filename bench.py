@@ -4,8 +4,15 @@
 Workload (N=1): BASELINE config 4 -- 4096 members x 4096 P1 elements, fp64,
 adaptive mask (|eta/d| > 1e-3), mixed solitary / box-uplift members.  A
 "step" is one time step of every member.  W untimed warm-up steps, then K
-timed steps in one fused launch (members stay resident in shared memory
-across steps; the 805 MB state is larger than L2).
+timed steps of the streaming path (four kernels per step: K_P predictor +
+criterion, K_S condensation, K_X tile chain, K_C reconstruction; the 805 MB
+state is far larger than the 126 MB L2, so every step streams it from HBM).
+
+Roofline: the dominant kernel is K_P.  Its algorithmic traffic is the state
+read + write, 96 B per cell; its average launch time is
+measured live with CUDA events recorded between the launches inside the
+timed region (nh_stream_timing), and `traffic` is the DRAM bytes per K_P
+launch from the committed `ncu --set full` capture (profiles/kp_traffic.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
                     [--workload config4|config5] [--mode adaptive|global]
@@ -35,6 +42,16 @@ sys.path.insert(0, ROOT)
 
 BYTES_PER_CELL_STEP = 96          # read + write of 6 fp64 state values
 METRIC = "cell-steps/sec (ensemble x cells x steps) incl. NH correction"
+
+
+def _kp_traffic():
+    """DRAM bytes (read + write) per K_P launch from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "kp_traffic.json")) as f:
+            d = json.load(f)
+        return float(d["dram_bytes_per_launch"]), d
+    except Exception:
+        return None, None
 
 
 def _peaks():
@@ -242,6 +259,7 @@ def run_b200(args):
     if world > 1:
         tdist.init_process_group("nccl")
     from paper_2505_17025_b200 import Criterion, Ensemble, _lib
+    from paper_2505_17025_b200 import _device as D
     from paper_2505_17025_b200._device import read_status
     cfg, recs, h, hu, hw = build_workload(args.workload, rank, world)
     B, N = h.shape[0], h.shape[1]
@@ -251,17 +269,23 @@ def run_b200(args):
     ens.advance(args.warmup, args.mode, crit)
     torch.cuda.synchronize()
     ens.reset_status()
+    path = ens.choose_path(args.mode, crit)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         tdist.barrier()
     torch.cuda.synchronize()
+    D.stream_timing(path == "stream")
+    n_launch0 = D.launch_count()
     with ClockSampler(local) as clk:
         ev0.record()
-        ens.advance(args.steps, args.mode, crit)
+        ens.advance(args.steps, args.mode, crit, path=path)
         ev1.record()
         ev1.synchronize()
     ms = ev0.elapsed_time(ev1)
     torch.cuda.synchronize()
+    launches = D.launch_count() - n_launch0
+    ktimes = D.stream_kernel_times() if path == "stream" else {}
+    D.stream_timing(False)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
@@ -276,32 +300,48 @@ def run_b200(args):
     cells = B * N * args.steps * world
     value = cells / (ms * 1e-3)
     peak, _, peak_kind = _peaks()
-    achieved = BYTES_PER_CELL_STEP * B * N * args.steps / (ms * 1e-3) / 1e9
+    if path == "stream":
+        kp_ms, kp_n = ktimes["nh_stream_kp"]
+        kp_avg = kp_ms / max(kp_n, 1)
+        kname = "nh_stream_kp"
+    else:   # resident path: one launch covers every step
+        kp_avg, kp_n, kname = ms / max(args.steps, 1), args.steps, "nh_step_kernel (per step)"
+    kp_bytes = BYTES_PER_CELL_STEP * B * N
+    achieved = kp_bytes / (kp_avg * 1e-3) / 1e9
+    traffic, traffic_src = _kp_traffic()
+    shares = {k: {"ms_total": v[0], "launches": v[1], "share": v[0] / ms}
+              for k, v in ktimes.items() if v[1]}
 
-    # end to end through the public API: host (pinned) -> device, K steps, device -> host
+    # end to end through the public API: pinned host state -> device, K steps
+    # (Ensemble.advance -> nh_stream_advance), device -> pinned host, timed on
+    # the wall clock around synchronizes (the larger of wall and event time).
     e2e = None
     if args.e2e:
         hh = [x.cpu().pin_memory() for x in (h, hu, hw)]
+        ho = [torch.empty_like(x).pin_memory() for x in hh]
         torch.cuda.synchronize()
         if world > 1:
             tdist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
         e0.record()
         dh = [x.to("cuda", non_blocking=True) for x in hh]
         ens2 = Ensemble(recs, *dh)
         ens2.advance(args.steps, args.mode, crit)
-        outs = [x.to("cpu", non_blocking=True) for x in (ens2.h, ens2.hu, ens2.hw)]
+        for dst, src in zip(ho, (ens2.h, ens2.hu, ens2.hw)):
+            dst.copy_(src, non_blocking=True)
         e1.record()
         e1.synchronize()
-        ems = e0.elapsed_time(e1)
+        ems = max(e0.elapsed_time(e1), (time.perf_counter() - w0) * 1e3)
         if world > 1:
             t = torch.tensor([ems], device="cuda")
             tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
             ems = float(t.item())
         nbytes = sum(x.numel() * 8 for x in hh)
         e2e = {"value": cells / (ems * 1e-3), "unit": "cell-steps/s",
-               "h2d_bytes_per_step": nbytes / args.steps, "d2h_bytes_per_step": nbytes / args.steps}
-        del dh, ens2, outs
+               "h2d_bytes_per_step": nbytes / args.steps, "d2h_bytes_per_step": nbytes / args.steps,
+               "call": "Ensemble(host state -> HBM).advance(K) -> host, one call per K steps"}
+        del dh, ens2, ho
 
     cpu = None
     if rank == 0 and world == 1 and args.cpu_steps > 0:
@@ -315,15 +355,21 @@ def run_b200(args):
             "config": {"workload": args.workload, "mode": args.mode, "members": B * world,
                        "cells_per_member": N, "members_per_gpu": B,
                        "criterion": "eta_over_d k_nh=1e-3", "mask_fraction": frac,
-                       "l2": "state 805 MB/GPU > 126 MB L2; one fused launch per timed region",
+                       "path": path,
+                       "l2": "inputs > L2: state 805 MB/GPU vs 126 MB L2, streamed every step",
                        "status_ok": ok, "errors": errors},
-            "gpu_launches": 1,
+            "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak,
+                         "traffic": traffic if path == "stream" else None,
+                         "kernel": kname, "kernel_ms_avg": kp_avg, "kernel_launches": kp_n,
+                         "algorithmic_bytes_per_launch": kp_bytes,
                          "peak_kind": peak_kind,
-                         "note": "algorithmic 96 B/cell-step; state is SMEM-resident across "
-                                 "the launch, so the binding roof is the fp64 pipe (see "
-                                 "profiles/)"},
+                         "traffic_source": traffic_src.get("source") if traffic_src else None,
+                         "note": "algorithmic 96 B/cell (state read + write) x B*N cells per "
+                                 "launch / event-timed launch; K_P is fp64-issue bound, "
+                                 "not HBM bound (profiles/)"},
+            "kernel_shares": shares,
             "clocks": clk.summary(),
         }
         if e2e:

@@ -134,17 +134,32 @@ int nh_advance(const nh_member* members, int n_members, int n_elements,
 
 /* Streaming variant of nh_advance for large ensembles (same contract and
  * in-place semantics; modes HYDROSTATIC / GLOBAL / ADAPTIVE with the
- * eta_over_d, eta_x, u, u_x criteria).  Every step is three kernels over
- * independent 248-element tiles (predictor+criterion+condensation, per-member
- * tile chain, reconstruction) with the vertical-momentum update fused into
- * the next step's load; state goes through HBM once per step.  `workspace`
- * is device memory of at least nh_stream_workspace_bytes(B, N) bytes. */
+ * eta_over_d, eta_x, u, u_x criteria).  Every step is four kernels over
+ * independent 248-element tiles (K_P predictor+criterion, K_S condensation,
+ * K_X per-member tile chain, K_C reconstruction) with the vertical-momentum
+ * update fused into the next step's load; state goes through HBM once per
+ * step.  `workspace` is device memory of at least
+ * nh_stream_workspace_bytes(B, N) bytes. */
 int nh_stream_advance(const nh_member* members, int n_members, int n_elements,
                       double* h, double* hu, double* hw, double* time, int n_steps,
                       const nh_scheme* scheme, const nh_outputs* outputs,
                       nh_status* status, void* workspace, size_t workspace_bytes,
                       void* stream);
 size_t nh_stream_workspace_bytes(int n_members, int n_elements);
+
+/* Per-kernel CUDA-event timing of nh_stream_advance (diagnostics for the
+ * roofline report).  nh_stream_timing(1) clears and arms the recorder; every
+ * later nh_stream_advance brackets each launch with events on its stream.
+ * nh_stream_kernel_times waits for the last event and returns, per kernel
+ * [K_P, K_S, K_X, K_C, finalising K_P], the summed milliseconds and launch
+ * counts since arming, then clears (timing stays armed until
+ * nh_stream_timing(0)). */
+#define NH_STREAM_NKERNELS 5
+int nh_stream_timing(int enable);
+int nh_stream_kernel_times(double* ms, long long* launches);
+
+/* Number of kernels this library has enqueued since load (all entry points). */
+long long nh_launch_count(void);
 
 /* Semi-discrete tendency, hydrostatic.rhs_operator (hydrostatic.py:88-184).
  * Outputs t_h, t_hu, t_hw [B][N][2]. */

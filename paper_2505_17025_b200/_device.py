@@ -200,3 +200,25 @@ def stream_advance(members, h, hu, hw, time, n_steps, sch, status, workspace, fl
                                int(n_steps), ctypes.byref(sch), ctypes.byref(out), ptr(status),
                                ptr(workspace), workspace.numel(), stream_ptr())
     _lib.check(rc, "nh_stream_advance")
+
+
+STREAM_KERNELS = ("nh_stream_kp", "nh_stream_ks", "nh_stream_kx", "nh_stream_kc",
+                  "nh_stream_kp_finalize")
+
+
+def stream_timing(enable: bool):
+    """Arm / disarm per-kernel CUDA-event timing inside nh_stream_advance."""
+    _lib.check(require_cuda().nh_stream_timing(1 if enable else 0), "nh_stream_timing")
+
+
+def stream_kernel_times() -> dict:
+    """{kernel: (total ms, launches)} recorded since arming (then cleared)."""
+    ms = (ctypes.c_double * 5)()
+    n = (ctypes.c_longlong * 5)()
+    _lib.check(require_cuda().nh_stream_kernel_times(ms, n), "nh_stream_kernel_times")
+    return {k: (ms[i], n[i]) for i, k in enumerate(STREAM_KERNELS)}
+
+
+def launch_count() -> int:
+    """Kernels the library has enqueued since it was loaded."""
+    return int(require_cuda().nh_launch_count())

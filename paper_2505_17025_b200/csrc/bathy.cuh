@@ -184,6 +184,51 @@ __device__ __forceinline__ Bottom6 bottom_eval(const nh_member& m, const BottomT
   return b;
 }
 
+// Time-independent part of a node's depth for the predictor: the smoothed
+// box's profile S(x) and S'(x) (everything but zeta(t)), so the two Heun
+// stages of a step evaluate the profile once.  Other kinds carry nothing.
+struct BottomSpace {
+  double S, Sx;
+  bool on;
+};
+
+template <int KIND>
+__device__ __forceinline__ BottomSpace bottom_space(const nh_member& m, double x) {
+  BottomSpace sp{0.0, 0.0, false};
+  if (KIND == NH_BOTTOM_SMOOTH_BOX) {
+    const double* p = m.bottom;
+    double y = RDIV(RSUB(fabs(x), p[2]), p[4]);
+    if (y < NH_BOX_YCUT) {
+      double E = exp(RMUL(-2.0, fabs(y)));
+      double inv1 = RDIV(1.0, RADD(1.0, E));
+      sp.S = y >= 0.0 ? RMUL(E, inv1) : inv1;
+      double sg = x >= 0.0 ? 1.0 : -1.0;
+      double sech2 = RMUL(RMUL(RMUL(4.0, E), inv1), inv1);
+      sp.Sx = RDIV(RMUL(RMUL(-0.5, sech2), sg), p[4]);
+      sp.on = true;
+    }
+  }
+  return sp;
+}
+
+// d and d_x at time factor bt from a precomputed BottomSpace; bit-identical
+// to bottom_eval<KIND, false>(m, bt, x).
+template <int KIND>
+__device__ __forceinline__ Bottom6 bottom_eval_sp(const nh_member& m, const BottomTime& bt,
+                                                  double x, const BottomSpace& sp) {
+  if (KIND == NH_BOTTOM_SMOOTH_BOX) {
+    const double* p = m.bottom;
+    Bottom6 b{p[0], 0.0, 0.0, 0.0, 0.0, 0.0};
+    if (sp.on) {
+      double zeta = RMUL(p[1], RSUB(1.0, bt.a));
+      b.d = RSUB(p[0], RMUL(zeta, sp.S));
+      b.d_x = RMUL(-zeta, sp.Sx);
+    }
+    return b;
+  }
+  return bottom_eval<KIND, false>(m, bt, x);
+}
+
 template <bool NEED_ALL = true>
 __device__ __forceinline__ Bottom6 bottom_eval_rt(const nh_member& m, const BottomTime& bt,
                                                   double x) {

@@ -2,7 +2,9 @@
 // geometry, cluster launches.
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <atomic>
 #include <mutex>
+#include <vector>
 #include <cstdlib>
 #include "step_kernel.cuh"
 #include "stream_kernels.cuh"
@@ -78,6 +80,52 @@ Plan make_plan(int n, int members) {
 bool g_attr_done = false;
 long long* g_prof = nullptr;
 std::mutex g_attr_mu;
+std::atomic<long long> g_launches{0};   // kernels this library has enqueued (nh_launch_count)
+
+// Optional per-kernel CUDA-event timing of the streaming path (nh_stream_timing):
+// one event between consecutive launches on the caller's stream, so event i-1 -> i
+// brackets exactly one kernel.
+struct StreamTiming {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  size_t used = 0;
+  struct Mark { int kernel; size_t a, b; };
+  std::vector<Mark> marks;
+  cudaEvent_t next() {
+    if (used == ev.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+      ev.push_back(e);
+    }
+    return ev[used++];
+  }
+} g_timing;
+std::mutex g_timing_mu;
+
+int counted(int rc) {
+  if (rc == 0) ++g_launches;
+  return rc;
+}
+
+// enqueue a plain launch of a streaming kernel, bracketing it with events when timing
+int stream_launch(void* k, int kid, dim3 g, dim3 b, void** args, cudaStream_t s) {
+  size_t a = 0;
+  if (g_timing.on) {
+    if (g_timing.used == 0 || g_timing.marks.empty() || g_timing.marks.back().b != g_timing.used - 1) {
+      cudaEvent_t e = g_timing.next();
+      if (!e || cudaEventRecord(e, s) != cudaSuccess) return NH_E_CUDA;
+    }
+    a = g_timing.used - 1;
+  }
+  if (cudaLaunchKernel(k, g, b, args, 0, s) != cudaSuccess) return NH_E_CUDA;
+  ++g_launches;
+  if (g_timing.on) {
+    cudaEvent_t e = g_timing.next();
+    if (!e || cudaEventRecord(e, s) != cudaSuccess) return NH_E_CUDA;
+    g_timing.marks.push_back({kid, a, g_timing.used - 1});
+  }
+  return 0;
+}
 
 int set_attrs() {
   std::lock_guard<std::mutex> lk(g_attr_mu);
@@ -158,32 +206,32 @@ int nh_advance(const nh_member* members, int n_members, int n_elements, double* 
   a.B = n_members; a.N = n_elements; a.n_steps = n_steps;
   a.cluster = p.cluster; a.tile = p.tile; a.nwords = (n_elements + 31) / 32;
   a.prof = g_prof;
-  return launch_cluster(nh_step_kernel_ptr(variant()), &a, n_members * p.cluster, p.threads, p.smem,
-                        p.cluster, (cudaStream_t)stream);
+  return counted(launch_cluster(nh_step_kernel_ptr(variant()), &a, n_members * p.cluster,
+                                p.threads, p.smem, p.cluster, (cudaStream_t)stream));
 }
 
 int nh_rhs(const nh_member* members, int n_members, int n_elements, const double* h,
            const double* hu, const double* hw, const double* time, double g, double* t_h,
            double* t_hu, double* t_hw, nh_status* status, void* stream) {
   if (!members || n_members < 1 || n_elements < 2) return NH_E_ARG;
-  return nh_launch_rhs(members, n_members, n_elements, h, hu, hw, time, g, t_h, t_hu, t_hw, status,
-                       (cudaStream_t)stream);
+  return counted(nh_launch_rhs(members, n_members, n_elements, h, hu, hw, time, g, t_h, t_hu, t_hw, status,
+                       (cudaStream_t)stream));
 }
 
 int nh_criterion(const nh_member* members, int n_members, int n_elements, const double* h,
                  const double* hu, const double* hw, const double* time, int kind,
                  double* values, void* stream) {
   if (!members || n_members < 1 || n_elements < 2 || kind < 0 || kind > 5) return NH_E_ARG;
-  return nh_launch_criterion(members, n_members, n_elements, h, hu, hw, time, kind, values,
-                             (cudaStream_t)stream);
+  return counted(nh_launch_criterion(members, n_members, n_elements, h, hu, hw, time, kind, values,
+                             (cudaStream_t)stream));
 }
 
 int nh_coefficients(const nh_member* members, int n_members, int n_elements, const double* h,
                     const double* hu, const double* hw, const double* time, double g, double rho,
                     double* coef, void* stream) {
   if (!members || n_members < 1 || n_elements < 2) return NH_E_ARG;
-  return nh_launch_coef(members, n_members, n_elements, h, hu, hw, time, g, rho, coef,
-                        (cudaStream_t)stream);
+  return counted(nh_launch_coef(members, n_members, n_elements, h, hu, hw, time, g, rho, coef,
+                        (cudaStream_t)stream));
 }
 
 int nh_ldg_solve(const nh_member* members, int n_members, int n_elements, const double* coef,
@@ -203,22 +251,22 @@ int nh_ldg_solve(const nh_member* members, int n_members, int n_elements, const 
   a.p = p; a.hu = hu; a.status = status; a.rho = rho; a.c11 = c11;
   a.B = n_members; a.N = n_elements; a.cluster = c; a.tile = tile;
   a.nwords = (n_elements + 31) / 32;
-  return launch_cluster(nh_solve_kernel_ptr(kE), &a, n_members * c, thr, nh_solve_smem_bytes(thr),
-                        c, (cudaStream_t)stream);
+  return counted(launch_cluster(nh_solve_kernel_ptr(kE), &a, n_members * c, thr,
+                                nh_solve_smem_bytes(thr), c, (cudaStream_t)stream));
 }
 
 int nh_correct_momentum(const nh_member* members, int n_members, int n_elements, const double* h,
                         const double* p, const double* coef, const uint32_t* flags, double rho,
                         const double* hw_in, double* hw_out, void* stream) {
   if (!members || n_members < 1 || n_elements < 2) return NH_E_ARG;
-  return nh_launch_momentum(members, n_members, n_elements, h, p, coef, flags, rho, hw_in, hw_out,
-                            (cudaStream_t)stream);
+  return counted(nh_launch_momentum(members, n_members, n_elements, h, p, coef, flags, rho, hw_in, hw_out,
+                            (cudaStream_t)stream));
 }
 
 int nh_bottom_sample(const nh_member* members, int n_members, const double* x, int n_points,
                      const double* time, double* out, void* stream) {
   if (!members || n_members < 1 || n_points < 0) return NH_E_ARG;
-  return nh_launch_bottom(members, n_members, x, n_points, time, out, (cudaStream_t)stream);
+  return counted(nh_launch_bottom(members, n_members, x, n_points, time, out, (cudaStream_t)stream));
 }
 
 // ------------------------------------------------------------- streaming path
@@ -280,10 +328,11 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
     a.pend_out = pend[k & 1];
     a.flags_cur = flags[k & 1];
     void* args[1] = {&a};
-    if (cudaLaunchKernel(kp, gp, bp, args, 0, s) != cudaSuccess) return NH_E_CUDA;
-    if (corr && cudaLaunchKernel(ks, gp, bp, args, 0, s) != cudaSuccess) return NH_E_CUDA;
-    if (cudaLaunchKernel(kx, gx, bx, args, 0, s) != cudaSuccess) return NH_E_CUDA;
-    if (corr && cudaLaunchKernel(kc, gp, bp, args, 0, s) != cudaSuccess) return NH_E_CUDA;
+    int rc = stream_launch(kp, 0, gp, bp, args, s);
+    if (!rc && corr) rc = stream_launch(ks, 1, gp, bp, args, s);
+    if (!rc) rc = stream_launch(kx, 2, gx, bx, args, s);
+    if (!rc && corr) rc = stream_launch(kc, 3, gp, bp, args, s);
+    if (rc) return rc;
     cur ^= 1;
   }
   double** fin = cur ? Bb : A;
@@ -293,7 +342,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
     a.flags_prev = flags[(n_steps - 1) & 1];
     a.finalize = 1;
     void* args[1] = {&a};
-    if (cudaLaunchKernel(kp, gp, bp, args, 0, s) != cudaSuccess) return NH_E_CUDA;
+    if (int rc = stream_launch(kp, 4, gp, bp, args, s)) return rc;
   }
   if (cur) {
     for (int f = 0; f < 3; ++f)
@@ -304,9 +353,40 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
     // gather p from the pending record of the last step where its flag is set
     const int last = (n_steps - 1) & 1;
     if (nh_launch_gather_p(pend[last], flags[last], outputs->p_nh, BN, s)) return NH_E_CUDA;
+    ++g_launches;
   }
   return 0;
 }
+
+int nh_stream_timing(int enable) {
+  std::lock_guard<std::mutex> lk(g_timing_mu);
+  g_timing.on = enable != 0;
+  g_timing.used = 0;
+  g_timing.marks.clear();
+  return 0;
+}
+
+int nh_stream_kernel_times(double* ms, long long* launches) {
+  std::lock_guard<std::mutex> lk(g_timing_mu);
+  for (int k = 0; k < NH_STREAM_NKERNELS; ++k) {
+    if (ms) ms[k] = 0.0;
+    if (launches) launches[k] = 0;
+  }
+  if (g_timing.used && cudaEventSynchronize(g_timing.ev[g_timing.used - 1]) != cudaSuccess)
+    return NH_E_CUDA;
+  for (const auto& m : g_timing.marks) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, g_timing.ev[m.a], g_timing.ev[m.b]) != cudaSuccess)
+      return NH_E_CUDA;
+    if (ms) ms[m.kernel] += t;
+    if (launches) launches[m.kernel] += 1;
+  }
+  g_timing.used = 0;
+  g_timing.marks.clear();
+  return 0;
+}
+
+long long nh_launch_count(void) { return g_launches.load(); }
 
 // diagnostics: device buffer [grid][NH_NPHASE] for NH_PROFILE_PHASES builds
 void nh_set_profile_buffer(long long* buf) { g_prof = buf; }

@@ -40,7 +40,7 @@ NH_DEV Side make_side(double h, double hu, double hw, double d) {
 #else
   s.rh = nh_rcp(h);
 #endif
-  s.u = RDIV(hu, h);
+  s.u = RDIVP(hu, h);
   return s;
 }
 
@@ -71,8 +71,8 @@ NH_DEV Face face_flux(const Side& L, const Side& R, double g, double& speed) {
   double F2 = RSUB(RMUL(0.5, s2), RMUL(lam, RSUB(qR, qL)));
 #if NH_STRICT
   // (hLs / hL) hwL is exactly hwL when hLs == hL (IEEE x / x == 1)
-  double wL = (hLs == L.h) ? L.hw : RMUL(RDIV(hLs, L.h), L.hw);
-  double wR = (hRs == R.h) ? R.hw : RMUL(RDIV(hRs, R.h), R.hw);
+  double wL = (hLs == L.h) ? L.hw : RMUL(RDIVP(hLs, L.h), L.hw);
+  double wR = (hRs == R.h) ? R.hw : RMUL(RDIVP(hRs, R.h), R.hw);
 #else
   double wL = (hLs == L.h) ? L.hw : (hLs * L.rh) * L.hw;
   double wR = (hRs == R.h) ? R.hw : (hRs * R.rh) * R.hw;

@@ -274,7 +274,7 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
               case NH_CRIT_ETA_OVER_D: {
                 double d0 = bot<KIND, false>(m, bt1, sample_xd(m, e0d + k, 0)).d;
                 double d1 = bot<KIND, false>(m, bt1, sample_xd(m, e0d + k, 1)).d;
-                v0 = fabs(RDIV(RSUB(h0, d0), d0)); v1 = fabs(RDIV(RSUB(h1, d1), d1));
+                v0 = fabs(RDIVP(RSUB(h0, d0), d0)); v1 = fabs(RDIVP(RSUB(h1, d1), d1));
                 break;
               }
               case NH_CRIT_ETA_X: {
@@ -285,22 +285,22 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
                 break;
               }
               case NH_CRIT_U:
-                v0 = fabs(RDIV(fld(sm.Qn, S, F_Q0, j), h0));
-                v1 = fabs(RDIV(fld(sm.Qn, S, F_Q1, j), h1));
+                v0 = fabs(RDIVP(fld(sm.Qn, S, F_Q0, j), h0));
+                v1 = fabs(RDIVP(fld(sm.Qn, S, F_Q1, j), h1));
                 break;
               case NH_CRIT_U_X: {
-                double u0 = RDIV(fld(sm.Qn, S, F_Q0, j), h0);
-                double u1 = RDIV(fld(sm.Qn, S, F_Q1, j), h1);
+                double u0 = RDIVP(fld(sm.Qn, S, F_Q0, j), h0);
+                double u1 = RDIVP(fld(sm.Qn, S, F_Q1, j), h1);
                 v0 = fabs(elem_deriv(m, u0, u1, 0)); v1 = fabs(elem_deriv(m, u0, u1, 1));
                 break;
               }
               case NH_CRIT_W:
-                v0 = fabs(RDIV(fld(sm.Qn, S, F_W0, j), h0));
-                v1 = fabs(RDIV(fld(sm.Qn, S, F_W1, j), h1));
+                v0 = fabs(RDIVP(fld(sm.Qn, S, F_W0, j), h0));
+                v1 = fabs(RDIVP(fld(sm.Qn, S, F_W1, j), h1));
                 break;
               default: {
-                double w0 = RDIV(fld(sm.Qn, S, F_W0, j), h0);
-                double w1 = RDIV(fld(sm.Qn, S, F_W1, j), h1);
+                double w0 = RDIVP(fld(sm.Qn, S, F_W0, j), h0);
+                double w1 = RDIVP(fld(sm.Qn, S, F_W1, j), h1);
                 v0 = fabs(elem_deriv(m, w0, w1, 0)); v1 = fabs(elem_deriv(m, w0, w1, 1));
                 break;
               }

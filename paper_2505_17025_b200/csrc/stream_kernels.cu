@@ -48,21 +48,29 @@ struct Q6 {
 // right face from the right neighbour's left face (exchanged through smem)
 template <int KIND>
 __device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q6& q,
-                                           const BottomTime& bt, double x0, double x1, int i,
+                                           const BottomTime& bt, double x0, double x1,
+                                           const BottomSpace& s0, const BottomSpace& s1, int i,
                                            int e, int N, double* sh, double* sf, double t6[6],
-                                           double& speed) {
-  Bottom6 b0 = bottom_eval<KIND, false>(m, bt, x0);
-  Bottom6 b1 = bottom_eval<KIND, false>(m, bt, x1);
+                                           double& speed, double& d0, double& d1) {
+  Bottom6 b0 = bottom_eval_sp<KIND>(m, bt, x0, s0);
+  Bottom6 b1 = bottom_eval_sp<KIND>(m, bt, x1, s1);
   Side n0 = make_side(q.h0, q.q0, q.w0, b0.d);
   Side n1 = make_side(q.h1, q.q1, q.w1, b1.d);
   sh[0 * TPB + i] = q.h1; sh[1 * TPB + i] = q.q1; sh[2 * TPB + i] = q.w1; sh[3 * TPB + i] = b1.d;
+  sh[4 * TPB + i] = n1.u;
   __syncthreads();
   Side L;
   if (e == 0) {
     L = ghost_side(n0, m.bc_left);
-  } else {
+  } else {   // the left neighbour's node-1 side, u included (no second division)
     int k = i > 0 ? i - 1 : 0;
-    L = make_side(sh[0 * TPB + k], sh[1 * TPB + k], sh[2 * TPB + k], sh[3 * TPB + k]);
+    L.h = sh[0 * TPB + k]; L.hu = sh[1 * TPB + k]; L.hw = sh[2 * TPB + k];
+    L.d = sh[3 * TPB + k]; L.u = sh[4 * TPB + k];
+#if NH_STRICT
+    L.rh = 0.0;
+#else
+    L.rh = nh_rcp(L.h);
+#endif
   }
   double sp;
   Face fl = face_flux(L, n0, g, sp);
@@ -78,6 +86,7 @@ __device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q
     fr.F1 = sf[0 * TPB + k]; fr.F2L = sf[1 * TPB + k]; fr.F3 = sf[2 * TPB + k]; fr.F2R = 0.0;
   }
   element_tendency(m, g, n0, n1, fl, fr, b0.d_x, b1.d_x, t6);
+  d0 = b0.d; d1 = b1.d;
 }
 
 __device__ __forceinline__ void store_super(double* dst, const Super& s) {
@@ -118,11 +127,12 @@ __device__ __forceinline__ Super tile_up(Super agg, bool tflag, double* wnode, d
 
 // ---------------------------------------------------------------------- K_P
 struct KpSmem {
-  double sh[4 * TPB];
+  double sh[5 * TPB];
   double sf[3 * TPB];
   double sk[6 * TPB];     // k1 of this thread's element
   double sq[6 * TPB];     // step-start state of this thread's element
-  double cfl;
+  double cfl;             // max wave speed of the tile (CFL = speed dt / dx at the end)
+  BottomTime bt[2];       // bottom time factors at t and t + dt (once per CTA)
   uint8_t rf[TPB];
 };
 
@@ -133,90 +143,45 @@ struct KsSmem {
   int wflag[NW];
 };
 
+// Per-thread geometry of a streaming tile.
+struct TileIdx {
+  int b, tile, i, lane, warp, e;
+  bool valid, own;
+  size_t o;
+};
+
+__device__ __forceinline__ TileIdx tile_idx(const StreamArgs& a) {
+  TileIdx t;
+  t.b = blockIdx.x / a.tiles; t.tile = blockIdx.x % a.tiles;
+  t.i = threadIdx.x; t.lane = t.i & 31; t.warp = t.i >> 5;
+  t.e = t.tile * OWN - H + t.i;
+  t.valid = t.e >= 0 && t.e < a.N;
+  t.own = t.valid && t.i >= H && t.i < H + OWN;
+  t.o = ((size_t)t.b * a.N + (t.valid ? t.e : 0)) * 2;
+  return t;
+}
+
 template <int KIND>
-__device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
-                                        const LdgConst& lk, KpSmem& ks) {
+__device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m, const TileIdx& ti,
+                                        Q6 q, KpSmem& ks) {
   double* sh = ks.sh;
   double* sf = ks.sf;
   uint8_t* rf = ks.rf;
   double& cfl_sh = ks.cfl;
 
   const int N = a.N, T = a.tiles;
-  const int b = blockIdx.x / T, tile = blockIdx.x % T;
-  const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
-  const int e = tile * OWN - H + i;
-  const bool valid = e >= 0 && e < N;
-  const bool own = valid && i >= H && i < H + OWN;
-  const size_t o = ((size_t)b * N + (valid ? e : 0)) * 2;
+  const int b = ti.b, tile = ti.tile, i = ti.i, lane = ti.lane, e = ti.e;
+  const bool valid = ti.valid, own = ti.own;
+  const size_t o = ti.o;
   const nh_scheme& sch = a.sch;
   const double g = sch.g;
   nh_status* st = a.status + b;
   const int step = a.step_counter ? a.step_counter[b] : 0;
-  if (i == 0) cfl_sh = 0.0;
 
-  // ---------------- load (coalesced double2 per field) ----------------
-  Q6 q{1.0, 1.0, 0.0, 0.0, 0.0, 0.0};
-  if (valid) {
-    double2 vh = *reinterpret_cast<const double2*>(a.h_in + o);
-    double2 vq = *reinterpret_cast<const double2*>(a.hu_in + o);
-    double2 vw = *reinterpret_cast<const double2*>(a.hw_in + o);
-    q = Q6{vh.x, vh.y, vq.x, vq.y, vw.x, vw.y};
-  }
-
-  // ---------------- pending correction of the previous step ----------------
-  // hw += dt/rho (6/quad p + d_x/quad (h p)_x + phi) on flagged elements
-  // (corrector.py:441-482); (h p)_x lifts use the neighbours' (h p) traces.
-  if (a.pend) {
-    const bool f = valid && a.flags_prev[(size_t)b * N + e];
-    double p0 = 0.0, p1 = 0.0, phi0 = 0.0, phi1 = 0.0, dx0 = 0.0, dx1 = 0.0;
-    if (f) {
-      const double* pv = a.pend + ((size_t)b * N + e) * 6;
-      p0 = pv[0]; p1 = pv[1]; phi0 = pv[2]; phi1 = pv[3]; dx0 = pv[4]; dx1 = pv[5];
-    }
-    double hp0 = q.h0 * p0, hp1 = q.h1 * p1;
-    sh[0 * TPB + i] = hp0;
-    sh[1 * TPB + i] = hp1;
-    __syncthreads();
-    if (f) {
-      auto hp_of = [&](int ee, int node, int slot) -> double {
-        if (slot >= 0 && slot < TPB) return sh[node * TPB + slot];
-        // neighbour outside the CTA's slots (never needed for own elements)
-        if (!a.flags_prev[(size_t)b * N + ee]) return 0.0;
-        size_t oo = ((size_t)b * N + ee) * 2 + node;
-        return a.h_in[oo] * a.pend[((size_t)b * N + ee) * 6 + node];
-      };
-      double hx0 = ederiv(m, hp0, hp1, 0), hx1 = ederiv(m, hp0, hp1, 1);
-      if (e < N - 1) {
-        double hr = hp_of(e + 1, 0, i + 1);
-        double avg = 0.5 * (hp1 + hr);
-        hx0 += (avg - hp1) * m.lift_right[0];
-        hx1 += (avg - hp1) * m.lift_right[1];
-      }
-      if (e > 0) {
-        double hl = hp_of(e - 1, 1, i - 1);
-        double avg = 0.5 * (hl + hp0);
-        hx0 -= (avg - hp0) * m.lift_left[0];
-        hx1 -= (avg - hp0) * m.lift_left[1];
-      }
-      double qd0 = 4.0 + dx0 * dx0, qd1 = 4.0 + dx1 * dx1;
-      double bp0 = nh_div(6.0, qd0) * p0 + nh_div(dx0, qd0) * hx0 + phi0;
-      double bp1 = nh_div(6.0, qd1) * p1 + nh_div(dx1, qd1) * hx1 + phi1;
-      q.w0 += lk.cdt * bp0;
-      q.w1 += lk.cdt * bp1;
-    }
-    __syncthreads();
-  }
-  if (a.finalize) {
-    if (own) {
-      double2 vw{q.w0, q.w1};
-      *reinterpret_cast<double2*>(const_cast<double*>(a.hw_in) + o) = vw;
-    }
-    return;
-  }
-
-  const double t = a.time[b], dt = m.dt, t1 = t + dt;
+  const double dt = m.dt;
   const double ed = (double)e;
   const double x0 = sample_xd(m, ed, 0), x1 = sample_xd(m, ed, 1);
+  const BottomSpace s0 = bottom_space<KIND>(m, x0), s1 = bottom_space<KIND>(m, x1);
   double speed = 0.0;
 
   // ---------------- Heun stage 1 at t ----------------
@@ -225,9 +190,8 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   ks.sq[3 * TPB + i] = q.q1; ks.sq[4 * TPB + i] = q.w0; ks.sq[5 * TPB + i] = q.w1;
   Q6 qs;
   {
-    BottomTime bt0 = bottom_time_k<KIND>(m, t);
-    double k1[6];
-    stage_tend<KIND>(m, g, q, bt0, x0, x1, i, e, N, sh, sf, k1, speed);
+    double k1[6], dd0, dd1;
+    stage_tend<KIND>(m, g, q, ks.bt[0], x0, x1, s0, s1, i, e, N, sh, sf, k1, speed, dd0, dd1);
 #pragma unroll
     for (int f = 0; f < 6; ++f) ks.sk[f * TPB + i] = k1[f];
     qs = Q6{RADD(q.h0, RMUL(dt, k1[0])), RADD(q.h1, RMUL(dt, k1[1])),
@@ -238,11 +202,10 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   __syncthreads();   // every read of sh / sf of stage 1 is done
 
   // ---------------- Heun stage 2 at t + dt ----------------
-  BottomTime bt1 = bottom_time_k<KIND>(m, t1);
-  double k2[6];
+  double k2[6], d0, d1;   // d0, d1: depth at t + dt, reused by the criterion
   {
     double dummy = 0.0;
-    stage_tend<KIND>(m, g, qs, bt1, x0, x1, i, e, N, sh, sf, k2, dummy);
+    stage_tend<KIND>(m, g, qs, ks.bt[1], x0, x1, s0, s1, i, e, N, sh, sf, k2, dummy, d0, d1);
   }
   double qv[6];
 #pragma unroll
@@ -255,16 +218,27 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
     *reinterpret_cast<double2*>(a.hu_out + o) = double2{qp.q0, qp.q1};
     *reinterpret_cast<double2*>(a.hw_out + o) = double2{qp.w0, qp.w1};
   }
-  if (sch.record_cfl) {   // all lanes take part in the shuffles (halo lanes contribute 0)
-    double c = own ? speed * dt / m.dx : 0.0;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) c = fmax(c, __shfl_down_sync(0xffffffffu, c, off));
-    if (lane == 0) atomicMax((unsigned long long*)&cfl_sh, (unsigned long long)__double_as_longlong(c));
+  if (sch.record_cfl) {
+    // max wave speed over the warp on the bit patterns (speeds are >= 0, so
+    // the unsigned order is the numeric order): high words, then low words of
+    // the lanes holding the maximal high word.  Halo lanes contribute 0.
+    const unsigned long long u = (unsigned long long)__double_as_longlong(own ? speed : 0.0);
+    const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(u >> 32));
+    const unsigned lo = __reduce_max_sync(0xffffffffu, (unsigned)(u >> 32) == hi ? (unsigned)u : 0u);
+    if (lane == 0 && (hi | lo))
+      atomicMax((unsigned long long*)&cfl_sh, ((unsigned long long)hi << 32) | lo);
   }
+  // CFL of the tile = (max speed) dt / dx: rounding is monotone, so this is
+  // the max over elements of the per-element speed dt / dx (hydrostatic.py CFL check)
+  auto publish_cfl = [&]() {
+    if (i == 0 && cfl_sh > 0.0) {
+      const double c = cfl_sh * dt / m.dx;
+      atomicMax((unsigned long long*)&st->cfl_max, (unsigned long long)__double_as_longlong(c));
+    }
+  };
   if (sch.mode == NH_MODE_HYDROSTATIC) {
     __syncthreads();
-    if (i == 0 && cfl_sh > 0.0)
-      atomicMax((unsigned long long*)&st->cfl_max, (unsigned long long)__double_as_longlong(cfl_sh));
+    publish_cfl();
     return;
   }
 
@@ -277,31 +251,27 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
       double v0, v1;
       switch (sch.criterion) {
         case NH_CRIT_ETA_OVER_D: {
-          double d0 = bottom_eval<KIND, false>(m, bt1, x0).d;
-          double d1 = bottom_eval<KIND, false>(m, bt1, x1).d;
-          v0 = fabs(RDIV(RSUB(qp.h0, d0), d0)); v1 = fabs(RDIV(RSUB(qp.h1, d1), d1));
+          v0 = fabs(RDIVP(RSUB(qp.h0, d0), d0)); v1 = fabs(RDIVP(RSUB(qp.h1, d1), d1));
           break;
         }
         case NH_CRIT_ETA_X: {
-          double d0 = bottom_eval<KIND, false>(m, bt1, x0).d;
-          double d1 = bottom_eval<KIND, false>(m, bt1, x1).d;
           v0 = fabs(ederiv(m, RSUB(qp.h0, d0), RSUB(qp.h1, d1), 0));
           v1 = fabs(ederiv(m, RSUB(qp.h0, d0), RSUB(qp.h1, d1), 1));
           break;
         }
         case NH_CRIT_U:
-          v0 = fabs(RDIV(qp.q0, qp.h0)); v1 = fabs(RDIV(qp.q1, qp.h1));
+          v0 = fabs(RDIVP(qp.q0, qp.h0)); v1 = fabs(RDIVP(qp.q1, qp.h1));
           break;
         case NH_CRIT_U_X: {
-          double u0 = RDIV(qp.q0, qp.h0), u1 = RDIV(qp.q1, qp.h1);
+          double u0 = RDIVP(qp.q0, qp.h0), u1 = RDIVP(qp.q1, qp.h1);
           v0 = fabs(ederiv(m, u0, u1, 0)); v1 = fabs(ederiv(m, u0, u1, 1));
           break;
         }
         case NH_CRIT_W:
-          v0 = fabs(RDIV(qp.w0, qp.h0)); v1 = fabs(RDIV(qp.w1, qp.h1));
+          v0 = fabs(RDIVP(qp.w0, qp.h0)); v1 = fabs(RDIVP(qp.w1, qp.h1));
           break;
         default: {
-          double w0 = RDIV(qp.w0, qp.h0), w1 = RDIV(qp.w1, qp.h1);
+          double w0 = RDIVP(qp.w0, qp.h0), w1 = RDIVP(qp.w1, qp.h1);
           v0 = fabs(ederiv(m, w0, w1, 0)); v1 = fabs(ederiv(m, w0, w1, 1));
           break;
         }
@@ -344,8 +314,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
       a.tile_agg[((size_t)b * T + tile) * 8 + 7] = (m.bc_right == NH_BC_WALL) ? -qq : qq;
     }
   }
-  if (i == 0 && cfl_sh > 0.0)
-    atomicMax((unsigned long long*)&st->cfl_max, (unsigned long long)__double_as_longlong(cfl_sh));
+  publish_cfl();
 }
 
 // ---------------------------------------------------------------------- K_S
@@ -354,7 +323,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
 // tile's merged super-element for K_X.
 template <int KIND>
 __device__ __forceinline__ void ks_body(const StreamArgs& a, const nh_member& m,
-                                        const LdgConst& lk, KsSmem& ks) {
+                                        const LdgConst& lk, const BottomTime& bt1, KsSmem& ks) {
   const int N = a.N, T = a.tiles;
   const int b = blockIdx.x / T, tile = blockIdx.x % T;
   const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
@@ -369,8 +338,6 @@ __device__ __forceinline__ void ks_body(const StreamArgs& a, const nh_member& m,
   Super S = super_identity();
   if (own) S = super_gap(a.hu_out[o]);
   if (flag) {
-    const double t1 = a.time[b] + m.dt;
-    const BottomTime bt1 = bottom_time_k<KIND>(m, t1);
     const double ed = (double)e;
     const double x0 = sample_xd(m, ed, 0), x1 = sample_xd(m, ed, 1);
     double2 vh = *reinterpret_cast<const double2*>(a.h_out + o);
@@ -402,20 +369,24 @@ __global__ void __launch_bounds__(TPB) nh_stream_ks(StreamArgs a) {
   __shared__ nh_member msh;
   __shared__ LdgConst ksh;
   __shared__ KsSmem ks;
+  __shared__ BottomTime kbt;
   const int b = blockIdx.x / a.tiles;
   if (!(a.tile_agg[(size_t)blockIdx.x * 8 + 6] > 0.0)) return;   // no flagged element
   if (threadIdx.x < (int)(sizeof(nh_member) / 8))
     reinterpret_cast<unsigned long long*>(&msh)[threadIdx.x] =
         reinterpret_cast<const unsigned long long*>(a.members + b)[threadIdx.x];
   __syncthreads();
-  if (threadIdx.x == 0) ksh = make_ldg_const(msh.dt, a.sch.g, a.sch.rho);
+  if (threadIdx.x == 0) {
+    ksh = make_ldg_const(msh.dt, a.sch.g, a.sch.rho);
+    kbt = bottom_time(msh, a.time[b] + msh.dt);
+  }
   __syncthreads();
   switch (msh.bottom_kind) {
-    case NH_BOTTOM_FLAT: ks_body<NH_BOTTOM_FLAT>(a, msh, ksh, ks); break;
-    case NH_BOTTOM_PLATE: ks_body<NH_BOTTOM_PLATE>(a, msh, ksh, ks); break;
-    case NH_BOTTOM_QUARTIC_SLIDE: ks_body<NH_BOTTOM_QUARTIC_SLIDE>(a, msh, ksh, ks); break;
-    case NH_BOTTOM_SMOOTH_BOX: ks_body<NH_BOTTOM_SMOOTH_BOX>(a, msh, ksh, ks); break;
-    default: ks_body<NH_BOTTOM_SLOPE_SLIDE>(a, msh, ksh, ks); break;
+    case NH_BOTTOM_FLAT: ks_body<NH_BOTTOM_FLAT>(a, msh, ksh, kbt, ks); break;
+    case NH_BOTTOM_PLATE: ks_body<NH_BOTTOM_PLATE>(a, msh, ksh, kbt, ks); break;
+    case NH_BOTTOM_QUARTIC_SLIDE: ks_body<NH_BOTTOM_QUARTIC_SLIDE>(a, msh, ksh, kbt, ks); break;
+    case NH_BOTTOM_SMOOTH_BOX: ks_body<NH_BOTTOM_SMOOTH_BOX>(a, msh, ksh, kbt, ks); break;
+    default: ks_body<NH_BOTTOM_SLOPE_SLIDE>(a, msh, ksh, kbt, ks); break;
   }
 }
 
@@ -423,20 +394,88 @@ __global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(Stream
   __shared__ nh_member msh;
   __shared__ LdgConst ksh;
   __shared__ KpSmem ks;
-  const int b = blockIdx.x / a.tiles;
+  const TileIdx ti = tile_idx(a);
+  const int N = a.N, i = ti.i, b = ti.b, e = ti.e;
+
+  // state and the previous step's pending record are requested first so their
+  // latency overlaps the member-record copy and the per-CTA constants
+  Q6 q{1.0, 1.0, 0.0, 0.0, 0.0, 0.0};
+  if (ti.valid) {
+    double2 vh = *reinterpret_cast<const double2*>(a.h_in + ti.o);
+    double2 vq = *reinterpret_cast<const double2*>(a.hu_in + ti.o);
+    double2 vw = *reinterpret_cast<const double2*>(a.hw_in + ti.o);
+    q = Q6{vh.x, vh.y, vq.x, vq.y, vw.x, vw.y};
+  }
+  const bool f = a.pend && ti.valid && a.flags_prev[(size_t)b * N + e];
+  double p0 = 0.0, p1 = 0.0, phi0 = 0.0, phi1 = 0.0, dx0 = 0.0, dx1 = 0.0;
+  if (f) {
+    const double* pv = a.pend + ((size_t)b * N + e) * 6;
+    p0 = pv[0]; p1 = pv[1]; phi0 = pv[2]; phi1 = pv[3]; dx0 = pv[4]; dx1 = pv[5];
+  }
   // cooperative copy of the 312-byte member record (one 8-byte word per thread)
-  if (threadIdx.x < (int)(sizeof(nh_member) / 8))
-    reinterpret_cast<unsigned long long*>(&msh)[threadIdx.x] =
-        reinterpret_cast<const unsigned long long*>(a.members + b)[threadIdx.x];
+  if (i < (int)(sizeof(nh_member) / 8))
+    reinterpret_cast<unsigned long long*>(&msh)[i] =
+        reinterpret_cast<const unsigned long long*>(a.members + b)[i];
+  const double hp0 = q.h0 * p0, hp1 = q.h1 * p1;
+  if (a.pend) {
+    ks.sh[0 * TPB + i] = hp0;
+    ks.sh[1 * TPB + i] = hp1;
+  }
+  if (i == 0) ks.cfl = 0.0;
   __syncthreads();
-  if (threadIdx.x == 0) ksh = make_ldg_const(msh.dt, a.sch.g, a.sch.rho);
-  __syncthreads();
+  // per-CTA constants on three different warps
+  if (i == 0) ksh = make_ldg_const(msh.dt, a.sch.g, a.sch.rho);
+  if (i == 32) ks.bt[0] = bottom_time(msh, a.time[b]);
+  if (i == 64) ks.bt[1] = bottom_time(msh, a.time[b] + msh.dt);
+
+  // ---------------- pending correction of the previous step ----------------
+  // hw += dt/rho (6/quad p + d_x/quad (h p)_x + phi) on flagged elements
+  // (corrector.py:441-482); (h p)_x lifts use the neighbours' (h p) traces.
+  double bp0 = 0.0, bp1 = 0.0;
+  if (f) {
+    const double* sh = ks.sh;
+    auto hp_of = [&](int ee, int node, int slot) -> double {
+      if (slot >= 0 && slot < TPB) return sh[node * TPB + slot];
+      // neighbour outside the CTA's slots (never needed for own elements)
+      if (!a.flags_prev[(size_t)b * N + ee]) return 0.0;
+      size_t oo = ((size_t)b * N + ee) * 2 + node;
+      return a.h_in[oo] * a.pend[((size_t)b * N + ee) * 6 + node];
+    };
+    double hx0 = ederiv(msh, hp0, hp1, 0), hx1 = ederiv(msh, hp0, hp1, 1);
+    if (e < N - 1) {
+      double hr = hp_of(e + 1, 0, i + 1);
+      double avg = 0.5 * (hp1 + hr);
+      hx0 += (avg - hp1) * msh.lift_right[0];
+      hx1 += (avg - hp1) * msh.lift_right[1];
+    }
+    if (e > 0) {
+      double hl = hp_of(e - 1, 1, i - 1);
+      double avg = 0.5 * (hl + hp0);
+      hx0 -= (avg - hp0) * msh.lift_left[0];
+      hx1 -= (avg - hp0) * msh.lift_left[1];
+    }
+    double qd0 = 4.0 + dx0 * dx0, qd1 = 4.0 + dx1 * dx1;
+    bp0 = nh_div(6.0, qd0) * p0 + nh_div(dx0, qd0) * hx0 + phi0;
+    bp1 = nh_div(6.0, qd1) * p1 + nh_div(dx1, qd1) * hx1 + phi1;
+  }
+  __syncthreads();   // constants visible; every read of the (h p) traces done
+  if (f) {
+    q.w0 += ksh.cdt * bp0;
+    q.w1 += ksh.cdt * bp1;
+  }
+  if (a.finalize) {
+    if (ti.own) {
+      double2 vw{q.w0, q.w1};
+      *reinterpret_cast<double2*>(const_cast<double*>(a.hw_in) + ti.o) = vw;
+    }
+    return;
+  }
   switch (msh.bottom_kind) {
-    case NH_BOTTOM_FLAT: kp_body<NH_BOTTOM_FLAT>(a, msh, ksh, ks); break;
-    case NH_BOTTOM_PLATE: kp_body<NH_BOTTOM_PLATE>(a, msh, ksh, ks); break;
-    case NH_BOTTOM_QUARTIC_SLIDE: kp_body<NH_BOTTOM_QUARTIC_SLIDE>(a, msh, ksh, ks); break;
-    case NH_BOTTOM_SMOOTH_BOX: kp_body<NH_BOTTOM_SMOOTH_BOX>(a, msh, ksh, ks); break;
-    default: kp_body<NH_BOTTOM_SLOPE_SLIDE>(a, msh, ksh, ks); break;
+    case NH_BOTTOM_FLAT: kp_body<NH_BOTTOM_FLAT>(a, msh, ti, q, ks); break;
+    case NH_BOTTOM_PLATE: kp_body<NH_BOTTOM_PLATE>(a, msh, ti, q, ks); break;
+    case NH_BOTTOM_QUARTIC_SLIDE: kp_body<NH_BOTTOM_QUARTIC_SLIDE>(a, msh, ti, q, ks); break;
+    case NH_BOTTOM_SMOOTH_BOX: kp_body<NH_BOTTOM_SMOOTH_BOX>(a, msh, ti, q, ks); break;
+    default: kp_body<NH_BOTTOM_SLOPE_SLIDE>(a, msh, ti, q, ks); break;
   }
 }
 

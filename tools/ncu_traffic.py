@@ -1,0 +1,45 @@
+"""DRAM traffic per launch of one kernel from an `ncu --set full` report ->
+profiles/kp_traffic.json (read by bench.py for roofline.traffic).
+
+usage: python tools/ncu_traffic.py rep.ncu-rep kernel_regex out.json
+"""
+import csv
+import io
+import json
+import re
+import subprocess
+import sys
+
+
+def main(rep, pattern, out):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+    tscale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "nsecond": 1e-6}
+    recs = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        if not re.search(pattern, d["Kernel Name"]):
+            continue
+        def val(k, table):
+            return float(d[k].replace(",", "")) * table[units[hdr.index(k)]]
+        recs.append({
+            "kernel": d["Kernel Name"], "grid": d["Grid Size"], "block": d["Block Size"],
+            "dram_read_bytes": val("dram__bytes_read.sum", scale),
+            "dram_write_bytes": val("dram__bytes_write.sum", scale),
+            "duration_ms": val("gpu__time_duration.sum", tscale),
+        })
+    r0 = recs[0]
+    res = {"source": rep.split("/")[-1], "kernel": r0["kernel"], "grid": r0["grid"],
+           "block": r0["block"],
+           "dram_bytes_per_launch": r0["dram_read_bytes"] + r0["dram_write_bytes"],
+           "dram_read_bytes": r0["dram_read_bytes"], "dram_write_bytes": r0["dram_write_bytes"],
+           "ncu_duration_ms": r0["duration_ms"], "launches_captured": len(recs)}
+    json.dump(res, open(out, "w"), indent=1)
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main(*sys.argv[1:4])
