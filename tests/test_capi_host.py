@@ -21,7 +21,7 @@ HEADER = os.path.join(ROOT, "include", "nhswe_b200.h")
 def header_functions():
     txt = open(HEADER).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return set(re.findall(r"^\s*(?:int|size_t|const char\*|void)\s+\**(nh_\w+)\s*\(", txt, flags=re.M))
+    return set(re.findall(r"^\s*(?:int|size_t|long long|const char\*|void)\s+\**(nh_\w+)\s*\(", txt, flags=re.M))
 
 
 def test_header_declares_the_exports():
