@@ -151,10 +151,10 @@ size_t nh_stream_workspace_bytes(int n_members, int n_elements);
  * roofline report).  nh_stream_timing(1) clears and arms the recorder; every
  * later nh_stream_advance brackets each launch with events on its stream.
  * nh_stream_kernel_times waits for the last event and returns, per kernel
- * [K_P, K_S, K_X, K_C, finalising K_P], the summed milliseconds and launch
+ * [K_P, K_S, K_X, K_C, finalising K_P, prep], the summed milliseconds and launch
  * counts since arming, then clears (timing stays armed until
  * nh_stream_timing(0)). */
-#define NH_STREAM_NKERNELS 5
+#define NH_STREAM_NKERNELS 6
 int nh_stream_timing(int enable);
 int nh_stream_kernel_times(double* ms, long long* launches);
 

@@ -203,7 +203,7 @@ def stream_advance(members, h, hu, hw, time, n_steps, sch, status, workspace, fl
 
 
 STREAM_KERNELS = ("nh_stream_kp", "nh_stream_ks", "nh_stream_kx", "nh_stream_kc",
-                  "nh_stream_kp_finalize")
+                  "nh_stream_kp_finalize", "nh_stream_prep")
 
 
 def stream_timing(enable: bool):
@@ -213,8 +213,8 @@ def stream_timing(enable: bool):
 
 def stream_kernel_times() -> dict:
     """{kernel: (total ms, launches)} recorded since arming (then cleared)."""
-    ms = (ctypes.c_double * 5)()
-    n = (ctypes.c_longlong * 5)()
+    ms = (ctypes.c_double * len(STREAM_KERNELS))()
+    n = (ctypes.c_longlong * len(STREAM_KERNELS))()
     _lib.check(require_cuda().nh_stream_kernel_times(ms, n), "nh_stream_kernel_times")
     return {k: (ms[i], n[i]) for i, k in enumerate(STREAM_KERNELS)}
 

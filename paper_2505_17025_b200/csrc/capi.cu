@@ -274,8 +274,8 @@ static int stream_tiles(int n) { return (n + NH_STREAM_OWN - 1) / NH_STREAM_OWN;
 
 size_t nh_stream_workspace_bytes(int n_members, int n_elements) {
   size_t BN = (size_t)n_members * n_elements, BT = (size_t)n_members * stream_tiles(n_elements);
-  size_t dbl = 6 * BN + 12 * BN + 12 * BN + 10 * BT;
-  return dbl * 8 + 2 * BN + 4 * (size_t)n_members + 1024;
+  size_t dbl = 6 * BN + 12 * BN + 12 * BN + 10 * BT + 16 * (size_t)n_members;
+  return dbl * 8 + 2 * BN + 4 * (size_t)n_members + 8 + 4 * BT + 1024;
 }
 
 int nh_stream_advance(const nh_member* members, int B, int N, double* h, double* hu, double* hw,
@@ -301,9 +301,27 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   double* pend[2] = {(double*)w, (double*)w + 6 * BN};  w += 12 * BN * 8;
   double* tagg = (double*)w;            w += 8 * BT * 8;
   double* tio = (double*)w;             w += 2 * BT * 8;
+  double* mconst = (double*)w;          w += 16 * (size_t)B * 8;
   uint8_t* flags[2] = {(uint8_t*)w, (uint8_t*)w + BN};  w += 2 * BN;
   int* counter = (int*)(((uintptr_t)w + 15) & ~(uintptr_t)15);
-  if (cudaMemsetAsync(counter, 0, 4 * (size_t)B, s) != cudaSuccess) return NH_E_CUDA;
+  int* tcount = counter + B;            // [2] flagged-tile counters (ping-pong by step)
+  int* tlist = tcount + 2;              // [B*T] flagged-tile list
+  if (cudaMemsetAsync(counter, 0, 4 * ((size_t)B + 2), s) != cudaSuccess) return NH_E_CUDA;
+  static int ks_grid = 0, kc_grid = 0;   // persistent grids: resident CTAs x SMs
+  if (!ks_grid) {
+    int dev = 0, sms = 0, nks = 0, nkc = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nks, nh_stream_kernel(3), NH_STREAM_THREADS, 0) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nkc, nh_stream_kernel(2), NH_STREAM_THREADS, 0) != cudaSuccess)
+      return NH_E_CUDA;
+    ks_grid = std::max(1, nks) * sms;
+    kc_grid = std::max(1, nkc) * sms;
+    if (const char* v = getenv("NH_KS_WAVES")) {   // diagnostics: grid = waves x resident CTAs
+      int wv = atoi(v);
+      if (wv > 0) { ks_grid *= wv; kc_grid *= wv; }
+    }
+  }
   double* A[3] = {h, hu, hw};
   double* Bb[3] = {alt, alt + 2 * BN, alt + 4 * BN};
   StreamArgs a = {};
@@ -311,12 +329,19 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   a.scratch = scratch; a.tile_agg = tagg; a.tile_io = tio;
   a.flag_bits = outputs ? outputs->flag_bits : nullptr;
   a.sch = sc; a.B = B; a.N = N; a.tiles = T; a.finalize = 0;
+  a.tile_list = tlist; a.mconst = mconst;
   const dim3 gp(B * T), bp(NH_STREAM_THREADS), gx((B + 7) / 8), bx(256);
+  const dim3 gs((unsigned)std::min<size_t>(ks_grid, BT)), gc((unsigned)std::min<size_t>(kc_grid, BT));
   void* kp = nh_stream_kernel(0);
   void* kx = nh_stream_kernel(1);
   void* kc = nh_stream_kernel(2);
   void* ks = nh_stream_kernel(3);
   const bool corr = sc.mode != NH_MODE_HYDROSTATIC;
+  {
+    void* args[1] = {&a};
+    if (int rc = stream_launch(nh_stream_kernel(4), 5, dim3((B + 255) / 256), dim3(256), args, s))
+      return rc;
+  }
   int cur = 0;   // 0: state in A, 1: state in Bb
   for (int k = 0; k < n_steps; ++k) {
     double** in = cur ? Bb : A;
@@ -327,11 +352,13 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
     a.flags_prev = flags[(k - 1) & 1];
     a.pend_out = pend[k & 1];
     a.flags_cur = flags[k & 1];
+    a.tile_count = tcount + (k & 1);
+    a.tile_count_next = tcount + ((k + 1) & 1);
     void* args[1] = {&a};
     int rc = stream_launch(kp, 0, gp, bp, args, s);
-    if (!rc && corr) rc = stream_launch(ks, 1, gp, bp, args, s);
+    if (!rc && corr) rc = stream_launch(ks, 1, gs, bp, args, s);
     if (!rc) rc = stream_launch(kx, 2, gx, bx, args, s);
-    if (!rc && corr) rc = stream_launch(kc, 3, gp, bp, args, s);
+    if (!rc && corr) rc = stream_launch(kc, 3, gc, bp, args, s);
     if (rc) return rc;
     cur ^= 1;
   }

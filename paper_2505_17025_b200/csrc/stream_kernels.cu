@@ -132,7 +132,6 @@ struct KpSmem {
   double sk[6 * TPB];     // k1 of this thread's element
   double sq[6 * TPB];     // step-start state of this thread's element
   double cfl;             // max wave speed of the tile (CFL = speed dt / dx at the end)
-  BottomTime bt[2];       // bottom time factors at t and t + dt (once per CTA)
   uint8_t rf[TPB];
 };
 
@@ -161,9 +160,44 @@ __device__ __forceinline__ TileIdx tile_idx(const StreamArgs& a) {
   return t;
 }
 
+// Per-member constants of one step, written once per member by K_X (for the
+// next step) or the prep kernel (first step) so tile kernels copy them with
+// the member record instead of recomputing them serially per CTA.
+struct MemberConst {
+  LdgConst lk;        // 8 doubles
+  BottomTime bt0;     // bottom time factors at t
+  BottomTime bt1;     // ... and at t + dt
+  double pad[2];
+};
+static_assert(sizeof(MemberConst) == 16 * 8, "MemberConst is 16 doubles");
+
+__device__ __forceinline__ void member_const(const nh_member& m, const nh_scheme& sch, double t,
+                                             double* out) {
+  MemberConst c;
+  c.lk = make_ldg_const(m.dt, sch.g, sch.rho);
+  c.bt0 = bottom_time(m, t);
+  c.bt1 = bottom_time(m, t + m.dt);
+  c.pad[0] = c.pad[1] = 0.0;
+  *reinterpret_cast<MemberConst*>(out) = c;
+}
+
+// cooperative copy of the member record (39 words) and its step constants (16)
+__device__ __forceinline__ void load_member(const StreamArgs& a, int b, nh_member& msh,
+                                            MemberConst& mc) {
+  constexpr int MW = (int)(sizeof(nh_member) / 8);
+  const int i = threadIdx.x;
+  if (i < MW)
+    reinterpret_cast<unsigned long long*>(&msh)[i] =
+        reinterpret_cast<const unsigned long long*>(a.members + b)[i];
+  else if (i < MW + 16)
+    reinterpret_cast<unsigned long long*>(&mc)[i - MW] =
+        reinterpret_cast<const unsigned long long*>(a.mconst + (size_t)b * 16)[i - MW];
+}
+
 template <int KIND>
-__device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m, const TileIdx& ti,
-                                        Q6 q, KpSmem& ks) {
+__device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
+                                        const MemberConst& mc, const TileIdx& ti, Q6 q,
+                                        KpSmem& ks) {
   double* sh = ks.sh;
   double* sf = ks.sf;
   uint8_t* rf = ks.rf;
@@ -191,7 +225,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   Q6 qs;
   {
     double k1[6], dd0, dd1;
-    stage_tend<KIND>(m, g, q, ks.bt[0], x0, x1, s0, s1, i, e, N, sh, sf, k1, speed, dd0, dd1);
+    stage_tend<KIND>(m, g, q, mc.bt0, x0, x1, s0, s1, i, e, N, sh, sf, k1, speed, dd0, dd1);
 #pragma unroll
     for (int f = 0; f < 6; ++f) ks.sk[f * TPB + i] = k1[f];
     qs = Q6{RADD(q.h0, RMUL(dt, k1[0])), RADD(q.h1, RMUL(dt, k1[1])),
@@ -205,7 +239,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   double k2[6], d0, d1;   // d0, d1: depth at t + dt, reused by the criterion
   {
     double dummy = 0.0;
-    stage_tend<KIND>(m, g, qs, ks.bt[1], x0, x1, s0, s1, i, e, N, sh, sf, k2, dummy, d0, d1);
+    stage_tend<KIND>(m, g, qs, mc.bt1, x0, x1, s0, s1, i, e, N, sh, sf, k2, dummy, d0, d1);
   }
   double qv[6];
 #pragma unroll
@@ -306,7 +340,10 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
       double* ta = a.tile_agg + ((size_t)b * T + tile) * 8;
       ta[6] = (double)nf;
       if (nf == 0) store_super(ta, super_gap(qp.q0));
-      if (nf) atomicAdd((unsigned long long*)&st->flagged, (unsigned long long)nf);
+      if (nf) {
+        atomicAdd((unsigned long long*)&st->flagged, (unsigned long long)nf);
+        a.tile_list[atomicAdd(a.tile_count, 1)] = blockIdx.x;   // work list of K_S / K_C
+      }
     }
     // right-end ghost outer trace (corrector.py:400-402)
     if (e == N - 1 && own) {
@@ -322,10 +359,10 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
 // condensation (corrector.py:100-349 -> physics.cuh), stored for K_C, and the
 // tile's merged super-element for K_X.
 template <int KIND>
-__device__ __forceinline__ void ks_body(const StreamArgs& a, const nh_member& m,
+__device__ __forceinline__ void ks_body(const StreamArgs& a, int bt, const nh_member& m,
                                         const LdgConst& lk, const BottomTime& bt1, KsSmem& ks) {
   const int N = a.N, T = a.tiles;
-  const int b = blockIdx.x / T, tile = blockIdx.x % T;
+  const int b = bt / T, tile = bt % T;
   const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
   const int e = tile * OWN - H + i;
   const bool valid = e >= 0 && e < N;
@@ -365,34 +402,33 @@ __device__ __forceinline__ void ks_body(const StreamArgs& a, const nh_member& m,
   if (i == 0) store_super(a.tile_agg + ((size_t)b * T + tile) * 8, v);
 }
 
+// Persistent: the grid strides over the step's list of flagged tiles (or over
+// every tile in global mode, where all are flagged and the list is skipped).
 __global__ void __launch_bounds__(TPB) nh_stream_ks(StreamArgs a) {
   __shared__ nh_member msh;
-  __shared__ LdgConst ksh;
+  __shared__ MemberConst mc;
   __shared__ KsSmem ks;
-  __shared__ BottomTime kbt;
-  const int b = blockIdx.x / a.tiles;
-  if (!(a.tile_agg[(size_t)blockIdx.x * 8 + 6] > 0.0)) return;   // no flagged element
-  if (threadIdx.x < (int)(sizeof(nh_member) / 8))
-    reinterpret_cast<unsigned long long*>(&msh)[threadIdx.x] =
-        reinterpret_cast<const unsigned long long*>(a.members + b)[threadIdx.x];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    ksh = make_ldg_const(msh.dt, a.sch.g, a.sch.rho);
-    kbt = bottom_time(msh, a.time[b] + msh.dt);
-  }
-  __syncthreads();
-  switch (msh.bottom_kind) {
-    case NH_BOTTOM_FLAT: ks_body<NH_BOTTOM_FLAT>(a, msh, ksh, kbt, ks); break;
-    case NH_BOTTOM_PLATE: ks_body<NH_BOTTOM_PLATE>(a, msh, ksh, kbt, ks); break;
-    case NH_BOTTOM_QUARTIC_SLIDE: ks_body<NH_BOTTOM_QUARTIC_SLIDE>(a, msh, ksh, kbt, ks); break;
-    case NH_BOTTOM_SMOOTH_BOX: ks_body<NH_BOTTOM_SMOOTH_BOX>(a, msh, ksh, kbt, ks); break;
-    default: ks_body<NH_BOTTOM_SLOPE_SLIDE>(a, msh, ksh, kbt, ks); break;
+  const bool all = a.sch.mode == NH_MODE_GLOBAL;
+  const int n = all ? a.B * a.tiles : *a.tile_count;
+  for (int w = blockIdx.x; w < n; w += gridDim.x) {
+    const int bt = all ? w : a.tile_list[w];
+    const int b = bt / a.tiles;
+    load_member(a, b, msh, mc);
+    __syncthreads();
+    switch (msh.bottom_kind) {
+      case NH_BOTTOM_FLAT: ks_body<NH_BOTTOM_FLAT>(a, bt, msh, mc.lk, mc.bt1, ks); break;
+      case NH_BOTTOM_PLATE: ks_body<NH_BOTTOM_PLATE>(a, bt, msh, mc.lk, mc.bt1, ks); break;
+      case NH_BOTTOM_QUARTIC_SLIDE: ks_body<NH_BOTTOM_QUARTIC_SLIDE>(a, bt, msh, mc.lk, mc.bt1, ks); break;
+      case NH_BOTTOM_SMOOTH_BOX: ks_body<NH_BOTTOM_SMOOTH_BOX>(a, bt, msh, mc.lk, mc.bt1, ks); break;
+      default: ks_body<NH_BOTTOM_SLOPE_SLIDE>(a, bt, msh, mc.lk, mc.bt1, ks); break;
+    }
+    __syncthreads();   // shared memory is reused by the next tile
   }
 }
 
 __global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(StreamArgs a) {
   __shared__ nh_member msh;
-  __shared__ LdgConst ksh;
+  __shared__ MemberConst mc;
   __shared__ KpSmem ks;
   const TileIdx ti = tile_idx(a);
   const int N = a.N, i = ti.i, b = ti.b, e = ti.e;
@@ -412,10 +448,7 @@ __global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(Stream
     const double* pv = a.pend + ((size_t)b * N + e) * 6;
     p0 = pv[0]; p1 = pv[1]; phi0 = pv[2]; phi1 = pv[3]; dx0 = pv[4]; dx1 = pv[5];
   }
-  // cooperative copy of the 312-byte member record (one 8-byte word per thread)
-  if (i < (int)(sizeof(nh_member) / 8))
-    reinterpret_cast<unsigned long long*>(&msh)[i] =
-        reinterpret_cast<const unsigned long long*>(a.members + b)[i];
+  load_member(a, b, msh, mc);
   const double hp0 = q.h0 * p0, hp1 = q.h1 * p1;
   if (a.pend) {
     ks.sh[0 * TPB + i] = hp0;
@@ -423,10 +456,6 @@ __global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(Stream
   }
   if (i == 0) ks.cfl = 0.0;
   __syncthreads();
-  // per-CTA constants on three different warps
-  if (i == 0) ksh = make_ldg_const(msh.dt, a.sch.g, a.sch.rho);
-  if (i == 32) ks.bt[0] = bottom_time(msh, a.time[b]);
-  if (i == 64) ks.bt[1] = bottom_time(msh, a.time[b] + msh.dt);
 
   // ---------------- pending correction of the previous step ----------------
   // hw += dt/rho (6/quad p + d_x/quad (h p)_x + phi) on flagged elements
@@ -458,10 +487,10 @@ __global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(Stream
     bp0 = nh_div(6.0, qd0) * p0 + nh_div(dx0, qd0) * hx0 + phi0;
     bp1 = nh_div(6.0, qd1) * p1 + nh_div(dx1, qd1) * hx1 + phi1;
   }
-  __syncthreads();   // constants visible; every read of the (h p) traces done
+  __syncthreads();   // every read of the (h p) traces done before sh is reused
   if (f) {
-    q.w0 += ksh.cdt * bp0;
-    q.w1 += ksh.cdt * bp1;
+    q.w0 += mc.lk.cdt * bp0;
+    q.w1 += mc.lk.cdt * bp1;
   }
   if (a.finalize) {
     if (ti.own) {
@@ -471,11 +500,11 @@ __global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(Stream
     return;
   }
   switch (msh.bottom_kind) {
-    case NH_BOTTOM_FLAT: kp_body<NH_BOTTOM_FLAT>(a, msh, ti, q, ks); break;
-    case NH_BOTTOM_PLATE: kp_body<NH_BOTTOM_PLATE>(a, msh, ti, q, ks); break;
-    case NH_BOTTOM_QUARTIC_SLIDE: kp_body<NH_BOTTOM_QUARTIC_SLIDE>(a, msh, ti, q, ks); break;
-    case NH_BOTTOM_SMOOTH_BOX: kp_body<NH_BOTTOM_SMOOTH_BOX>(a, msh, ti, q, ks); break;
-    default: kp_body<NH_BOTTOM_SLOPE_SLIDE>(a, msh, ti, q, ks); break;
+    case NH_BOTTOM_FLAT: kp_body<NH_BOTTOM_FLAT>(a, msh, mc, ti, q, ks); break;
+    case NH_BOTTOM_PLATE: kp_body<NH_BOTTOM_PLATE>(a, msh, mc, ti, q, ks); break;
+    case NH_BOTTOM_QUARTIC_SLIDE: kp_body<NH_BOTTOM_QUARTIC_SLIDE>(a, msh, mc, ti, q, ks); break;
+    case NH_BOTTOM_SMOOTH_BOX: kp_body<NH_BOTTOM_SMOOTH_BOX>(a, msh, mc, ti, q, ks); break;
+    default: kp_body<NH_BOTTOM_SLOPE_SLIDE>(a, msh, mc, ti, q, ks); break;
   }
 }
 
@@ -487,6 +516,7 @@ __global__ void __launch_bounds__(256) nh_stream_kx(StreamArgs a) {
   __shared__ double nodes[8][31 * 6];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * 8 + warp;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.tile_count_next) *a.tile_count_next = 0;
   if (b >= a.B) return;
   const int T = a.tiles;
   const int cpl = (T + 31) / 32;
@@ -517,22 +547,34 @@ __global__ void __launch_bounds__(256) nh_stream_kx(StreamArgs a) {
     }
   }
   if (lane == 0) {
-    a.time[b] = a.time[b] + a.members[b].dt;
+    const double tn = a.time[b] + a.members[b].dt;
+    a.time[b] = tn;
     if (a.step_counter) a.step_counter[b] += 1;
+    member_const(a.members[b], a.sch, tn, a.mconst + (size_t)b * 16);   // next step's constants
   }
 }
 
+// Step constants of every member at its current time (before the first step).
+__global__ void __launch_bounds__(256) nh_stream_prep(StreamArgs a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < a.B) member_const(a.members[b], a.sch, a.time[b], a.mconst + (size_t)b * 16);
+}
+
 // ---------------------------------------------------------------------- K_C
-__global__ void __launch_bounds__(TPB) nh_stream_kc(StreamArgs a) {
-  __shared__ double wnode[NW * 31 * 6];
-  __shared__ double wagg[NW * 6];
-  __shared__ double bnode[31 * 6];
-  __shared__ double wio[NW * 2];
-  __shared__ int wflag[NW];
+struct KcSmem {
+  double wnode[NW * 31 * 6];
+  double wagg[NW * 6];
+  double bnode[31 * 6];
+  double wio[NW * 2];
+};
+
+__device__ __forceinline__ void kc_tile(const StreamArgs& a, int bt, KcSmem& kc) {
+  double* wnode = kc.wnode;
+  double* wagg = kc.wagg;
+  double* bnode = kc.bnode;
+  double* wio = kc.wio;
   const int N = a.N, T = a.tiles;
-  const int b = blockIdx.x / T, tile = blockIdx.x % T;
-  const double* ta = a.tile_agg + ((size_t)b * T + tile) * 8;
-  if (!(ta[6] > 0.0)) return;                         // no flagged element in this tile
+  const int b = bt / T, tile = bt % T;
   const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
   const int e = tile * OWN - H + i;
   const bool valid = e >= 0 && e < N;
@@ -587,6 +629,17 @@ __global__ void __launch_bounds__(TPB) nh_stream_kc(StreamArgs a) {
   pn[1] = a.sch.rho * P1;
 }
 
+// Persistent: the grid strides over the step's list of flagged tiles.
+__global__ void __launch_bounds__(TPB) nh_stream_kc(StreamArgs a) {
+  __shared__ KcSmem kc;
+  const bool all = a.sch.mode == NH_MODE_GLOBAL;
+  const int n = all ? a.B * a.tiles : *a.tile_count;
+  for (int w = blockIdx.x; w < n; w += gridDim.x) {
+    kc_tile(a, all ? w : a.tile_list[w], kc);
+    __syncthreads();   // shared memory is reused by the next tile
+  }
+}
+
 __global__ void nh_gather_p_kernel(const double* pend, const uint8_t* flags, double* p, size_t n) {
   size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (k >= n) return;
@@ -606,6 +659,7 @@ void* nh_stream_kernel(int which) {
     case 0: return (void*)nh_stream_kp;
     case 1: return (void*)nh_stream_kx;
     case 3: return (void*)nh_stream_ks;
+    case 4: return (void*)nh_stream_prep;
     default: return (void*)nh_stream_kc;
   }
 }

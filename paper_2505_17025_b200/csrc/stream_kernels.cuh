@@ -31,10 +31,15 @@ struct StreamArgs {
   int* step_counter;           // [B] steps done in this call
   nh_status* status;
   uint32_t* flag_bits;         // optional [n_steps][B][nwords]
+  double* mconst;              // [B][16] per-member step constants (MemberConst)
+  int* tile_list;              // [B*T] tiles holding a flagged element (this step, any order)
+  int* tile_count;             // entries of tile_list (K_P appends, K_S / K_C consume)
+  int* tile_count_next;        // the next step's counter, zeroed by K_X
   nh_scheme sch;
   int B, N, tiles, finalize;
 };
 
+// which: 0 K_P, 1 K_X, 2 K_C, 3 K_S, 4 prep (step constants for the current time)
 void* nh_stream_kernel(int which);
 int nh_launch_gather_p(const double* pend, const uint8_t* flags, double* p, size_t n,
                        cudaStream_t s);
