@@ -81,7 +81,7 @@ typedef struct nh_member {
     double mass[4];
     double stiffness[4];
     double deriv_ref[4];
-    double bottom[12];      /* model parameters, see nh_pack_* in DESIGN.md */
+    double bottom[12];      /* model parameters, layout in csrc/bathy.cuh   */
     int32_t bc_left;        /* NH_BC_*                                      */
     int32_t bc_right;
     int32_t bottom_kind;    /* NH_BOTTOM_*                                  */
