@@ -404,7 +404,7 @@ __device__ __forceinline__ void ks_body(const StreamArgs& a, int bt, const nh_me
 
 // Persistent: the grid strides over the step's list of flagged tiles (or over
 // every tile in global mode, where all are flagged and the list is skipped).
-__global__ void __launch_bounds__(TPB) nh_stream_ks(StreamArgs a) {
+__global__ void __launch_bounds__(TPB, NH_KS_MIN_BLOCKS) nh_stream_ks(StreamArgs a) {
   __shared__ nh_member msh;
   __shared__ MemberConst mc;
   __shared__ KsSmem ks;
@@ -630,7 +630,7 @@ __device__ __forceinline__ void kc_tile(const StreamArgs& a, int bt, KcSmem& kc)
 }
 
 // Persistent: the grid strides over the step's list of flagged tiles.
-__global__ void __launch_bounds__(TPB) nh_stream_kc(StreamArgs a) {
+__global__ void __launch_bounds__(TPB, NH_KS_MIN_BLOCKS) nh_stream_kc(StreamArgs a) {
   __shared__ KcSmem kc;
   const bool all = a.sch.mode == NH_MODE_GLOBAL;
   const int n = all ? a.B * a.tiles : *a.tile_count;

@@ -4,13 +4,18 @@
 #include <stddef.h>
 #include "../../include/nhswe_b200.h"
 
+#ifndef NH_STREAM_THREADS
 #define NH_STREAM_THREADS 256
+#endif
 #define NH_STREAM_HALO 4
 #define NH_STREAM_OWN (NH_STREAM_THREADS - 2 * NH_STREAM_HALO)
-#define NH_STREAM_MAXCPL 8
+#define NH_STREAM_MAXCPL 8   // tiles per lane in K_X: members up to 32*8*OWN elements
 #ifndef NH_STREAM_MIN_BLOCKS
-#define NH_STREAM_MIN_BLOCKS 4
-#endif   // tiles per lane in K_X: members up to 32*8*248 elements
+#define NH_STREAM_MIN_BLOCKS (1024 / NH_STREAM_THREADS)   // K_P CTAs per SM (64 registers)
+#endif
+#ifndef NH_KS_MIN_BLOCKS
+#define NH_KS_MIN_BLOCKS (768 / NH_STREAM_THREADS)        // K_S / K_C CTAs per SM
+#endif
 
 struct StreamArgs {
   const nh_member* members;
