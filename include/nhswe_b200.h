@@ -161,6 +161,14 @@ int nh_stream_kernel_times(double* ms, long long* launches);
 /* Number of kernels this library has enqueued since load (all entry points). */
 long long nh_launch_count(void);
 
+/* Self-test of the inline correctly rounded division / square root used in
+ * the strict predictor against CUDA's __ddiv_rn / __dsqrt_rn on n random
+ * operand pairs (all exponent ranges, zeros, denormals, inf, nan).
+ * mismatches: device uint64[3] (division, sqrt, positive-divisor division),
+ * accumulated. */
+int nh_selftest_arith(long long n, unsigned long long seed, unsigned long long* mismatches,
+                      void* stream);
+
 /* Semi-discrete tendency, hydrostatic.rhs_operator (hydrostatic.py:88-184).
  * Outputs t_h, t_hu, t_hw [B][N][2]. */
 int nh_rhs(const nh_member* members, int n_members, int n_elements,

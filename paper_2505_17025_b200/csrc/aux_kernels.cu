@@ -260,7 +260,61 @@ template __global__ void nh_solve_kernel<3>(SolveArgs);
 void* nh_solve_kernel_ptr(int E) { return E == 3 ? (void*)nh_solve_kernel<3> : nullptr; }
 
 // ------------------------------------------------------------- launch helpers
+// ------------------------------------------------------------ arithmetic self-test
+__device__ __forceinline__ unsigned long long splitmix(unsigned long long& x) {
+  unsigned long long z = (x += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// operand with a mix of exponent ranges: mostly near 1 (the solver's values),
+// plus full-range, tiny, denormal, zero, huge, inf and nan operands
+__device__ __forceinline__ double test_operand(unsigned long long& st) {
+  unsigned long long r = splitmix(st);
+  unsigned cls = (unsigned)(r & 15);
+  unsigned long long mant = (r >> 4) & 0xfffffffffffffull;
+  unsigned long long sign = (r >> 60) & 1ull;
+  unsigned long long ex;
+  switch (cls) {
+    case 0: return sign ? -0.0 : 0.0;
+    case 1: ex = 0; break;                                        // denormal
+    case 2: ex = 1 + (splitmix(st) % 60); break;                   // tiny
+    case 3: ex = 2046 - (splitmix(st) % 60); break;                // huge
+    case 4: ex = (splitmix(st) & 1) ? 2047 : 1 + (splitmix(st) % 2046); break;  // inf/nan or any
+    case 5: case 6: ex = 1 + (splitmix(st) % 2046); break;         // full range
+    default: ex = 1023 - 40 + (splitmix(st) % 60); break;          // 1e-12 .. 1e6
+  }
+  return __longlong_as_double((long long)((sign << 63) | (ex << 52) | mant));
+}
+
+__device__ __forceinline__ bool same_bits(double x, double y) {
+  return __double_as_longlong(x) == __double_as_longlong(y) || (isnan(x) && isnan(y));
+}
+
+__global__ void nh_selftest_kernel(long long n, unsigned long long seed, unsigned long long* bad) {
+  unsigned long long nd = 0, ns = 0, np = 0;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    unsigned long long st = seed ^ ((unsigned long long)k * 0xd1b54a32d192ed03ull);
+    double a = test_operand(st), b = test_operand(st);
+    nd += !same_bits(nh_ddiv_rn(a, b), __ddiv_rn(a, b));
+    ns += !same_bits(nh_dsqrt_rn(a), __dsqrt_rn(a));
+    double bp = fabs(b);
+    if (bp > 0.0 && bp < INFINITY) np += !same_bits(nh_div_pos(a, bp), __ddiv_rn(a, bp));
+  }
+  if (nd) atomicAdd(bad + 0, nd);
+  if (ns) atomicAdd(bad + 1, ns);
+  if (np) atomicAdd(bad + 2, np);
+}
+
 extern "C" {
+
+int nh_launch_selftest(long long n, unsigned long long seed, unsigned long long* bad,
+                       cudaStream_t s) {
+  nh_selftest_kernel<<<148 * 8, 256, 0, s>>>(n, seed, bad);
+  return cudaGetLastError() == cudaSuccess ? 0 : NH_E_CUDA;
+}
 
 int nh_launch_rhs(const nh_member* members, int B, int N, const double* h, const double* hu,
                   const double* hw, const double* time, double g, double* th, double* tq,

@@ -229,6 +229,28 @@ __device__ __forceinline__ Bottom6 bottom_eval_sp(const nh_member& m, const Bott
   return bottom_eval<KIND, false>(m, bt, x);
 }
 
+// KIND = -1: run-time dispatch on m.bottom_kind (CTA-uniform in the
+// streaming kernels), one copy of the calling code instead of five
+template <int KIND>
+__device__ __forceinline__ BottomSpace bottom_space_k(const nh_member& m, double x) {
+  if (KIND >= 0) return bottom_space<KIND>(m, x);
+  if (m.bottom_kind == NH_BOTTOM_SMOOTH_BOX) return bottom_space<NH_BOTTOM_SMOOTH_BOX>(m, x);
+  return BottomSpace{0.0, 0.0, false};
+}
+
+template <int KIND>
+__device__ __forceinline__ Bottom6 bottom_eval_sp_k(const nh_member& m, const BottomTime& bt,
+                                                    double x, const BottomSpace& sp) {
+  if (KIND >= 0) return bottom_eval_sp<KIND>(m, bt, x, sp);
+  switch (m.bottom_kind) {
+    case NH_BOTTOM_PLATE: return bottom_eval_sp<NH_BOTTOM_PLATE>(m, bt, x, sp);
+    case NH_BOTTOM_QUARTIC_SLIDE: return bottom_eval_sp<NH_BOTTOM_QUARTIC_SLIDE>(m, bt, x, sp);
+    case NH_BOTTOM_SMOOTH_BOX: return bottom_eval_sp<NH_BOTTOM_SMOOTH_BOX>(m, bt, x, sp);
+    case NH_BOTTOM_SLOPE_SLIDE: return bottom_eval_sp<NH_BOTTOM_SLOPE_SLIDE>(m, bt, x, sp);
+    default: return bottom_eval_sp<NH_BOTTOM_FLAT>(m, bt, x, sp);
+  }
+}
+
 template <bool NEED_ALL = true>
 __device__ __forceinline__ Bottom6 bottom_eval_rt(const nh_member& m, const BottomTime& bt,
                                                   double x) {

@@ -16,6 +16,7 @@ int nh_launch_criterion(const nh_member*, int, int, const double*, const double*
                         const double*, int, double*, cudaStream_t);
 int nh_launch_coef(const nh_member*, int, int, const double*, const double*, const double*,
                    const double*, double, double, double*, cudaStream_t);
+int nh_launch_selftest(long long, unsigned long long, unsigned long long*, cudaStream_t);
 int nh_launch_bottom(const nh_member*, int, const double*, int, const double*, double*,
                      cudaStream_t);
 int nh_launch_momentum(const nh_member*, int, int, const double*, const double*, const double*,
@@ -414,6 +415,12 @@ int nh_stream_kernel_times(double* ms, long long* launches) {
 }
 
 long long nh_launch_count(void) { return g_launches.load(); }
+
+int nh_selftest_arith(long long n, unsigned long long seed, unsigned long long* mismatches,
+                      void* stream) {
+  if (n < 0 || !mismatches) return NH_E_ARG;
+  return counted(nh_launch_selftest(n, seed, mismatches, (cudaStream_t)stream));
+}
 
 // diagnostics: device buffer [grid][NH_NPHASE] for NH_PROFILE_PHASES builds
 void nh_set_profile_buffer(long long* buf) { g_prof = buf; }

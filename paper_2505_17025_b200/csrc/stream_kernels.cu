@@ -52,8 +52,8 @@ __device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q
                                            const BottomSpace& s0, const BottomSpace& s1, int i,
                                            int e, int N, double* sh, double* sf, double t6[6],
                                            double& speed, double& d0, double& d1) {
-  Bottom6 b0 = bottom_eval_sp<KIND>(m, bt, x0, s0);
-  Bottom6 b1 = bottom_eval_sp<KIND>(m, bt, x1, s1);
+  Bottom6 b0 = bottom_eval_sp_k<KIND>(m, bt, x0, s0);
+  Bottom6 b1 = bottom_eval_sp_k<KIND>(m, bt, x1, s1);
   Side n0 = make_side(q.h0, q.q0, q.w0, b0.d);
   Side n1 = make_side(q.h1, q.q1, q.w1, b1.d);
   sh[0 * TPB + i] = q.h1; sh[1 * TPB + i] = q.q1; sh[2 * TPB + i] = q.w1; sh[3 * TPB + i] = b1.d;
@@ -215,7 +215,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   const double dt = m.dt;
   const double ed = (double)e;
   const double x0 = sample_xd(m, ed, 0), x1 = sample_xd(m, ed, 1);
-  const BottomSpace s0 = bottom_space<KIND>(m, x0), s1 = bottom_space<KIND>(m, x1);
+  const BottomSpace s0 = bottom_space_k<KIND>(m, x0), s1 = bottom_space_k<KIND>(m, x1);
   double speed = 0.0;
 
   // ---------------- Heun stage 1 at t ----------------
@@ -499,6 +499,9 @@ __global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(Stream
     }
     return;
   }
+#if NH_KP_RUNTIME_KIND
+  kp_body<-1>(a, msh, mc, ti, q, ks);
+#else
   switch (msh.bottom_kind) {
     case NH_BOTTOM_FLAT: kp_body<NH_BOTTOM_FLAT>(a, msh, mc, ti, q, ks); break;
     case NH_BOTTOM_PLATE: kp_body<NH_BOTTOM_PLATE>(a, msh, mc, ti, q, ks); break;
@@ -506,6 +509,7 @@ __global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(Stream
     case NH_BOTTOM_SMOOTH_BOX: kp_body<NH_BOTTOM_SMOOTH_BOX>(a, msh, mc, ti, q, ks); break;
     default: kp_body<NH_BOTTOM_SLOPE_SLIDE>(a, msh, mc, ti, q, ks); break;
   }
+#endif
 }
 
 // ---------------------------------------------------------------------- K_X

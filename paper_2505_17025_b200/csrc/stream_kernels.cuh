@@ -13,6 +13,9 @@
 #ifndef NH_STREAM_MIN_BLOCKS
 #define NH_STREAM_MIN_BLOCKS (1024 / NH_STREAM_THREADS)   // K_P CTAs per SM (64 registers)
 #endif
+#ifndef NH_KP_RUNTIME_KIND
+#define NH_KP_RUNTIME_KIND 0   // 1: one K_P body with run-time bottom dispatch (smaller code)
+#endif
 #ifndef NH_KS_MIN_BLOCKS
 #define NH_KS_MIN_BLOCKS (768 / NH_STREAM_THREADS)        // K_S / K_C CTAs per SM
 #endif

@@ -224,3 +224,16 @@ def test_full_mask_adaptive_equals_global():
         assert ra.mask.fraction == 1.0
     assert np.abs(sa.hu.values - sg.hu.values).max() < 1e-12
     assert np.abs(sa.hw.values - sg.hw.values).max() < 1e-12
+
+
+def test_inline_ieee_division_and_sqrt_match_cuda():
+    """The strict predictor's inline division / sqrt (nh_common.cuh) are the
+    IEEE round-to-nearest results, bit-identical to __ddiv_rn / __dsqrt_rn."""
+    import torch
+    from paper_2505_17025_b200 import _device as D
+    lib = D.require_cuda()
+    bad = torch.zeros(3, dtype=torch.int64, device="cuda")
+    n = 1 << 30
+    assert lib.nh_selftest_arith(n, 20251020, bad.data_ptr(), D.stream_ptr()) == 0
+    torch.cuda.synchronize()
+    assert bad.tolist() == [0, 0, 0]
