@@ -512,6 +512,13 @@ def _band_system(grid, co: Coeffs, ranges, outer, c11, c12, c22):
         ab[6 + r - c, c] += v
 
     b = np.zeros(size)
+    # forcing products over the stacked ranges in ONE matmul, as the reference
+    # does (corrector.py:343-344): numpy's (n, 2) @ (2, 2) kernel rounds a
+    # 1-row operand differently from a many-row one, so per-range products
+    # would differ by an ulp on single-element ranges
+    stack = np.concatenate([np.arange(e0 - co.offset, e1 + 1 - co.offset) for e0, e1 in ranges])
+    f1M = ((co.f1[stack] / rho) @ M.T)
+    f2M = (co.f2[stack] @ M.T)
     base = 0
     for (e0, e1), (oL, oR) in zip(ranges, outer):
         idx = slice(e0 - co.offset, e1 + 1 - co.offset)
@@ -537,8 +544,8 @@ def _band_system(grid, co: Coeffs, ranges, outer, c11, c12, c22):
         put(Q[0, 0], P[0, 0], c11)
         put(Q[-1, 1], Q[-1, 1], 0.5 + c12)
         put(Q[-1, 1], P[-1, 1], c11)
-        b[P.ravel()] = ((co.f1[idx] / rho) @ M.T).ravel()
-        b[Q.ravel()] = (co.f2[idx] @ M.T).ravel()
+        b[P.ravel()] = f1M[base // 4:base // 4 + m].ravel()
+        b[Q.ravel()] = f2M[base // 4:base // 4 + m].ravel()
         b[Q[0, 0]] += (0.5 + c12) * oL
         b[Q[-1, 1]] -= (0.5 - c12) * oR
         base += 4 * m
