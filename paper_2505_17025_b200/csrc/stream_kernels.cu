@@ -43,6 +43,88 @@ struct Q6 {
   double h0, h1, q0, q1, w0, w1;
 };
 
+#if NH_KP_WARP_XCHG
+// Named-barrier handshakes between neighbouring warps (ids 1..2*(NW-1); 0 is
+// __syncthreads).  A(w): warp w's node-1 side is in smem for warp w+1.
+// B(w): warp w+1's left-face flux is in smem for warp w.
+__device__ __forceinline__ void bar_arrive(int id) {
+  asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory");
+}
+__device__ __forceinline__ void bar_wait(int id) {
+  asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+}
+#define NH_BAR_A(w) (1 + (w))
+#define NH_BAR_B(w) (NW + (w))
+
+// one Heun stage for the thread's element.  Neighbour exchange inside a warp
+// goes through shuffles; across a warp boundary through two small smem slots
+// per warp and a producer/consumer named barrier with that neighbour only, so
+// warps never wait for the whole CTA.
+template <int KIND>
+__device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q6& q,
+                                           const BottomTime& bt, double x0, double x1,
+                                           const BottomSpace& s0, const BottomSpace& s1, int i,
+                                           int e, int N, double* xs, double* xf, double t6[6],
+                                           double& speed, double& d0, double& d1) {
+  const int lane = i & 31, warp = i >> 5;
+  Bottom6 b0 = bottom_eval_sp_k<KIND>(m, bt, x0, s0);
+  Bottom6 b1 = bottom_eval_sp_k<KIND>(m, bt, x1, s1);
+  Side n0 = make_side(q.h0, q.q0, q.w0, b0.d);
+  Side n1 = make_side(q.h1, q.q1, q.w1, b1.d);
+  // left neighbour's node-1 side (u included: no second division)
+  Side L;
+  L.h = __shfl_up_sync(0xffffffffu, n1.h, 1);
+  L.hu = __shfl_up_sync(0xffffffffu, n1.hu, 1);
+  L.hw = __shfl_up_sync(0xffffffffu, n1.hw, 1);
+  L.d = __shfl_up_sync(0xffffffffu, n1.d, 1);
+  L.u = __shfl_up_sync(0xffffffffu, n1.u, 1);
+  if (lane == 31) {
+    double* x = xs + warp * 5;
+    x[0] = n1.h; x[1] = n1.hu; x[2] = n1.hw; x[3] = n1.d; x[4] = n1.u;
+  }
+  if (warp < NW - 1) bar_arrive(NH_BAR_A(warp));
+  if (warp > 0) {
+    bar_wait(NH_BAR_A(warp - 1));
+    if (lane == 0) {
+      const double* x = xs + (warp - 1) * 5;
+      L.h = x[0]; L.hu = x[1]; L.hw = x[2]; L.d = x[3]; L.u = x[4];
+    }
+  }
+#if NH_STRICT
+  L.rh = 0.0;
+#else
+  L.rh = nh_rcp(L.h);
+#endif
+  if (e == 0) L = ghost_side(n0, m.bc_left);
+  // (CTA slot 0 keeps lane 0's own value: a halo element, never used)
+  double sp;
+  Face fl = face_flux(L, n0, g, sp);
+  speed = fmax(speed, sp);
+  Face fr;
+  fr.F1 = __shfl_down_sync(0xffffffffu, fl.F1, 1);
+  fr.F2L = __shfl_down_sync(0xffffffffu, fl.F2L, 1);
+  fr.F3 = __shfl_down_sync(0xffffffffu, fl.F3, 1);
+  fr.F2R = 0.0;
+  if (lane == 0) {
+    double* y = xf + warp * 3;
+    y[0] = fl.F1; y[1] = fl.F2L; y[2] = fl.F3;
+  }
+  if (warp > 0) bar_arrive(NH_BAR_B(warp - 1));
+  if (warp < NW - 1) {
+    bar_wait(NH_BAR_B(warp));
+    if (lane == 31) {
+      const double* y = xf + (warp + 1) * 3;
+      fr.F1 = y[0]; fr.F2L = y[1]; fr.F3 = y[2];
+    }
+  }
+  if (e == N - 1) {
+    fr = face_flux(n1, ghost_side(n1, m.bc_right), g, sp);
+    speed = fmax(speed, sp);
+  }
+  element_tendency(m, g, n0, n1, fl, fr, b0.d_x, b1.d_x, t6);
+  d0 = b0.d; d1 = b1.d;
+}
+#else
 // one Heun stage for the thread's element: node sides from the registers,
 // left face from the left neighbour's node-1 side (exchanged through smem),
 // right face from the right neighbour's left face (exchanged through smem)
@@ -89,6 +171,8 @@ __device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q
   d0 = b0.d; d1 = b1.d;
 }
 
+#endif
+
 __device__ __forceinline__ void store_super(double* dst, const Super& s) {
   dst[0] = s.ga; dst[1] = s.aa; dst[2] = s.ba; dst[3] = s.gz; dst[4] = s.az; dst[5] = s.bz;
 }
@@ -127,8 +211,15 @@ __device__ __forceinline__ Super tile_up(Super agg, bool tflag, double* wnode, d
 
 // ---------------------------------------------------------------------- K_P
 struct KpSmem {
+#if NH_KP_WARP_XCHG
+  double sh[2 * TPB];     // (h p) traces of the pending correction
+  double sf[1];
+  double xs[NW * 5];      // per warp: node-1 side of its lane 31
+  double xf[NW * 3];      // per warp: left-face flux of its lane 0
+#else
   double sh[5 * TPB];
   double sf[3 * TPB];
+#endif
   double sk[6 * TPB];     // k1 of this thread's element
   double sq[6 * TPB];     // step-start state of this thread's element
   double cfl;             // max wave speed of the tile (CFL = speed dt / dx at the end)
@@ -201,6 +292,14 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   double* sh = ks.sh;
   double* sf = ks.sf;
   uint8_t* rf = ks.rf;
+#if NH_KP_WARP_XCHG
+  double* XS = ks.xs;
+  double* XF = ks.xf;
+  (void)sf;
+#else
+  double* XS = sh;
+  double* XF = sf;
+#endif
   double& cfl_sh = ks.cfl;
 
   const int N = a.N, T = a.tiles;
@@ -225,7 +324,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   Q6 qs;
   {
     double k1[6], dd0, dd1;
-    stage_tend<KIND>(m, g, q, mc.bt0, x0, x1, s0, s1, i, e, N, sh, sf, k1, speed, dd0, dd1);
+    stage_tend<KIND>(m, g, q, mc.bt0, x0, x1, s0, s1, i, e, N, XS, XF, k1, speed, dd0, dd1);
 #pragma unroll
     for (int f = 0; f < 6; ++f) ks.sk[f * TPB + i] = k1[f];
     qs = Q6{RADD(q.h0, RMUL(dt, k1[0])), RADD(q.h1, RMUL(dt, k1[1])),
@@ -233,13 +332,15 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
             RADD(q.w0, RMUL(dt, k1[4])), RADD(q.w1, RMUL(dt, k1[5]))};
   }
   if (own && !(qs.h0 > 0.0 && qs.h1 > 0.0)) nh_report(st, step, NH_ERR_POSITIVITY_STAGE1, -1);
+#if !NH_KP_WARP_XCHG
   __syncthreads();   // every read of sh / sf of stage 1 is done
+#endif
 
   // ---------------- Heun stage 2 at t + dt ----------------
   double k2[6], d0, d1;   // d0, d1: depth at t + dt, reused by the criterion
   {
     double dummy = 0.0;
-    stage_tend<KIND>(m, g, qs, mc.bt1, x0, x1, s0, s1, i, e, N, sh, sf, k2, dummy, d0, d1);
+    stage_tend<KIND>(m, g, qs, mc.bt1, x0, x1, s0, s1, i, e, N, XS, XF, k2, dummy, d0, d1);
   }
   double qv[6];
 #pragma unroll

@@ -16,6 +16,9 @@
 #ifndef NH_KP_RUNTIME_KIND
 #define NH_KP_RUNTIME_KIND 0   // 1: one K_P body with run-time bottom dispatch (smaller code)
 #endif
+#ifndef NH_KP_WARP_XCHG
+#define NH_KP_WARP_XCHG 0      // 1: K_P neighbour exchange by shuffles + warp-pair named barriers (measured slower)
+#endif
 #ifndef NH_KS_MIN_BLOCKS
 #define NH_KS_MIN_BLOCKS (768 / NH_STREAM_THREADS)        // K_S / K_C CTAs per SM
 #endif
