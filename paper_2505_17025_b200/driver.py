@@ -92,6 +92,19 @@ class Ensemble:
         tiles = self.B * ((self.N + 247) // 248)
         return "stream" if tiles >= 2 * 148 else "resident"
 
+    def stream_chunk(self, budget: int | None = None) -> int:
+        """Members per streaming launch sequence: the whole ensemble when its
+        workspace fits next to the state, else the largest block that does
+        (config 5 at full size: 51.5 GB of state, 4 MB of workspace per member)."""
+        if getattr(self, "_chunk", None) is None:
+            lib = D.require_cuda()
+            per = int(lib.nh_stream_workspace_bytes(1, self.N))
+            if budget is None:
+                free, _ = D.torch().cuda.mem_get_info()
+                budget = int(free * 0.85)
+            self._chunk = int(max(1, min(self.B, budget // per)))
+        return self._chunk
+
     def advance(self, n_steps: int, mode: str = "adaptive", criterion: Criterion | None = None,
                 flux: FluxCoefficients = FluxCoefficients(), g: float = 9.81,
                 rho: float = RHO_WATER, flag_bits=None, p_out=None, path: str = "auto"):
@@ -105,10 +118,25 @@ class Ensemble:
         if path == "auto":
             path = self.choose_path(mode, criterion)
         if path == "stream":
+            chunk = self.stream_chunk()
             if getattr(self, "_ws", None) is None:
-                self._ws = D.stream_workspace(self.B, self.N)
-            D.stream_advance(self.members, self.h, self.hu, self.hw, self.time, n_steps, sch,
-                             self.status, self._ws, flag_bits, p_out)
+                self._ws = D.stream_workspace(chunk, self.N)
+            if chunk >= self.B:
+                D.stream_advance(self.members, self.h, self.hu, self.hw, self.time, n_steps, sch,
+                                 self.status, self._ws, flag_bits, p_out)
+                return
+            # members are independent: run the ensemble as consecutive member
+            # blocks through one workspace (member-major state -> contiguous views)
+            if flag_bits is not None:
+                raise ValueError("per-step flag bits need the whole ensemble in one workspace")
+            mb, sb = self.members, self.status
+            rec, st = _lib.MEMBER_DTYPE.itemsize, _lib.STATUS_DTYPE.itemsize
+            for c0 in range(0, self.B, chunk):
+                c1 = min(self.B, c0 + chunk)
+                D.stream_advance(mb[c0 * rec:c1 * rec], self.h[c0:c1], self.hu[c0:c1],
+                                 self.hw[c0:c1], self.time[c0:c1], n_steps, sch,
+                                 sb[c0 * st:c1 * st], self._ws,
+                                 None, None if p_out is None else p_out[c0:c1])
         else:
             D.advance(self.members, self.h, self.hu, self.hw, self.time, n_steps, sch,
                       self.status, flag_bits, p_out)

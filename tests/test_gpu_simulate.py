@@ -153,3 +153,24 @@ def test_per_step_replay_after_long_run():
     assert bad.size == 0
     assert rel(r.state.h.values - 1.0, o.h - 1.0) <= 1e-12
     assert rel(r.state.hu.values, o.hu) <= 1e-12
+
+
+def test_stream_member_chunks_bitwise_equal():
+    """Ensembles too large for one workspace run as member blocks through one
+    workspace (config 5 at full size); results are identical to one block."""
+    cfg = configs.Config4(n_members=6, n_elements=700, n_steps=60)
+    recs = cfg.records()
+    states = [cfg.host_state(i, oracle_depth) for i in range(cfg.n_members)]
+    H, Q, W = (np.stack([s[k] for s in states]) for k in range(3))
+    out = []
+    for chunk in (None, 2, 4):
+        ens = P.Ensemble.from_host(recs, H, Q, W)
+        if chunk:
+            ens._chunk = chunk
+        ens.advance(cfg.n_steps, "adaptive", P.Criterion("eta_over_d"), path="stream")
+        st = ens.check()
+        out.append((ens.h.cpu().numpy(), ens.hu.cpu().numpy(), ens.hw.cpu().numpy(),
+                    ens.time.cpu().numpy(), st["flagged"].copy()))
+    for other in out[1:]:
+        for a, b in zip(out[0], other):
+            assert np.array_equal(a, b)
