@@ -307,9 +307,13 @@ def run_b200(args):
         kname = "nh_stream_kp"
     else:   # resident path: one launch covers every step
         kp_avg, kp_n, kname = ms / max(args.steps, 1), args.steps, "nh_step_kernel (per step)"
-    kp_bytes = BYTES_PER_CELL_STEP * B * N
+    # cells per K_P launch: the whole ensemble, or one member block when it is
+    # run in blocks (config 5 at full size)
+    kp_bytes = BYTES_PER_CELL_STEP * B * N * args.steps / max(kp_n, 1)
     achieved = kp_bytes / (kp_avg * 1e-3) / 1e9
     traffic, traffic_src = _kp_traffic()
+    if traffic_src and traffic_src.get("workload", "config4") != args.workload:
+        traffic, traffic_src = None, None     # the committed capture is of another shape
     shares = {k: {"ms_total": v[0], "launches": v[1], "share": v[0] / ms}
               for k, v in ktimes.items() if v[1]}
 

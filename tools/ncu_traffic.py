@@ -32,7 +32,7 @@ def main(rep, pattern, out):
             "duration_ms": val("gpu__time_duration.sum", tscale),
         })
     r0 = recs[0]
-    res = {"source": rep.split("/")[-1], "kernel": r0["kernel"], "grid": r0["grid"],
+    res = {"source": rep.split("/")[-1], "workload": "config4", "kernel": r0["kernel"], "grid": r0["grid"],
            "block": r0["block"],
            "dram_bytes_per_launch": r0["dram_read_bytes"] + r0["dram_write_bytes"],
            "dram_read_bytes": r0["dram_read_bytes"], "dram_write_bytes": r0["dram_write_bytes"],
