@@ -493,11 +493,15 @@ __device__ __forceinline__ void ks_body(const StreamArgs& a, int bt, const nh_me
     double R[6];
     if (!local_condense(m, c0, c1, lk.rho, lk.inv_rho, a.sch.c11, range_end, S, R))
       nh_report(st, step, NH_ERR_SOLVE_PIVOT, e);
-    double* sc = a.scratch + fe * 12;
-    store_super(sc, S);
-    sc[6] = R[0]; sc[7] = R[1]; sc[8] = R[2]; sc[9] = R[3]; sc[10] = R[4]; sc[11] = R[5];
-    double* pn = a.pend_out + fe * 6;
-    pn[2] = c0.phi; pn[3] = c1.phi; pn[4] = b0.d_x; pn[5] = b1.d_x;
+    // field-major planes: each store of the warp is one coalesced 256-byte run
+    const size_t BN = (size_t)a.B * N;
+    double* sc = a.scratch + fe;
+    sc[0 * BN] = S.ga; sc[1 * BN] = S.aa; sc[2 * BN] = S.ba;
+    sc[3 * BN] = S.gz; sc[4 * BN] = S.az; sc[5 * BN] = S.bz;
+#pragma unroll
+    for (int r = 0; r < 6; ++r) sc[(6 + r) * BN] = R[r];
+    double* pn = a.pend_out + fe;
+    pn[2 * BN] = c0.phi; pn[3 * BN] = c1.phi; pn[4 * BN] = b0.d_x; pn[5 * BN] = b1.d_x;
   }
   Super v = tile_up(S, flag, ks.wnode, ks.wagg, ks.bnode, ks.wflag, lane, warp);
   if (i == 0) store_super(a.tile_agg + ((size_t)b * T + tile) * 8, v);
@@ -546,8 +550,9 @@ __global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(Stream
   const bool f = a.pend && ti.valid && a.flags_prev[(size_t)b * N + e];
   double p0 = 0.0, p1 = 0.0, phi0 = 0.0, phi1 = 0.0, dx0 = 0.0, dx1 = 0.0;
   if (f) {
-    const double* pv = a.pend + ((size_t)b * N + e) * 6;
-    p0 = pv[0]; p1 = pv[1]; phi0 = pv[2]; phi1 = pv[3]; dx0 = pv[4]; dx1 = pv[5];
+    const size_t BN = (size_t)a.B * N;
+    const double* pv = a.pend + (size_t)b * N + e;
+    p0 = pv[0]; p1 = pv[BN]; phi0 = pv[2 * BN]; phi1 = pv[3 * BN]; dx0 = pv[4 * BN]; dx1 = pv[5 * BN];
   }
   load_member(a, b, msh, mc);
   const double hp0 = q.h0 * p0, hp1 = q.h1 * p1;
@@ -569,7 +574,7 @@ __global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(Stream
       // neighbour outside the CTA's slots (never needed for own elements)
       if (!a.flags_prev[(size_t)b * N + ee]) return 0.0;
       size_t oo = ((size_t)b * N + ee) * 2 + node;
-      return a.h_in[oo] * a.pend[((size_t)b * N + ee) * 6 + node];
+      return a.h_in[oo] * a.pend[(size_t)node * a.B * N + (size_t)b * N + ee];
     };
     double hx0 = ederiv(msh, hp0, hp1, 0), hx1 = ederiv(msh, hp0, hp1, 1);
     if (e < N - 1) {
@@ -689,9 +694,11 @@ __device__ __forceinline__ void kc_tile(const StreamArgs& a, int bt, KcSmem& kc)
   Super S = super_identity();
   double R[6] = {0, 0, 0, 0, 0, 0};
   if (flag) {
-    const double* sc = a.scratch + ((size_t)b * N + e) * 12;
-    S = load_super(sc);
-    R[0] = sc[6]; R[1] = sc[7]; R[2] = sc[8]; R[3] = sc[9]; R[4] = sc[10]; R[5] = sc[11];
+    const size_t BN = (size_t)a.B * N;
+    const double* sc = a.scratch + (size_t)b * N + e;
+    S = Super{sc[0], sc[BN], sc[2 * BN], sc[3 * BN], sc[4 * BN], sc[5 * BN]};
+#pragma unroll
+    for (int r = 0; r < 6; ++r) R[r] = sc[(6 + r) * BN];
   } else if (own) {
     S = super_gap(a.hu_out[o]);
   }
@@ -729,9 +736,9 @@ __device__ __forceinline__ void kc_tile(const StreamArgs& a, int bt, KcSmem& kc)
     nh_report(a.status + b, step, NH_ERR_SOLVE_NONFINITE, e);
   }
   *reinterpret_cast<double2*>(a.hu_out + o) = double2{Q0, Q1};
-  double* pn = a.pend_out + ((size_t)b * N + e) * 6;
+  double* pn = a.pend_out + (size_t)b * N + e;
   pn[0] = a.sch.rho * P0;
-  pn[1] = a.sch.rho * P1;
+  pn[(size_t)a.B * N] = a.sch.rho * P1;
 }
 
 // Persistent: the grid strides over the step's list of flagged tiles.
@@ -749,8 +756,8 @@ __global__ void nh_gather_p_kernel(const double* pend, const uint8_t* flags, dou
   size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (k >= n) return;
   bool f = flags[k];
-  p[2 * k] = f ? pend[6 * k] : 0.0;
-  p[2 * k + 1] = f ? pend[6 * k + 1] : 0.0;
+  p[2 * k] = f ? pend[k] : 0.0;             // planes p0, p1 of the pending record
+  p[2 * k + 1] = f ? pend[n + k] : 0.0;
 }
 
 int nh_launch_gather_p(const double* pend, const uint8_t* flags, double* p, size_t n,

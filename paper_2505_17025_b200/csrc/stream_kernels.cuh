@@ -33,9 +33,9 @@ struct StreamArgs {
   double* hw_out;
   const uint8_t* flags_prev;   // flags of the step whose correction is pending (or unused)
   uint8_t* flags_cur;
-  const double* pend;          // [B][N][6] p0 p1 phi0 phi1 dx0 dx1 of the pending step, or NULL
+  const double* pend;          // [6][B*N] planes p0 p1 phi0 phi1 dx0 dx1 of the pending step, or NULL
   double* pend_out;            // same, for this step
-  double* scratch;             // [B][N][12] super-element + reconstruction rows
+  double* scratch;             // [12][B*N] planes: super-element (6) + reconstruction rows (6)
   double* tile_agg;            // [B][T][8] aggregate (6), flagged count, right ghost
   double* tile_io;             // [B][T][2] (a_in, z_in)
   double* time;                // [B]
