@@ -331,7 +331,8 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   a.flag_bits = outputs ? outputs->flag_bits : nullptr;
   a.sch = sc; a.B = B; a.N = N; a.tiles = T; a.finalize = 0;
   a.tile_list = tlist; a.mconst = mconst;
-  const dim3 gp(B * T), bp(NH_STREAM_THREADS), gx((B + 7) / 8), bx(256);
+  const dim3 gp(T, std::min(B, 65535), (B + 65534) / 65535), bp(NH_STREAM_THREADS),
+      gx((B + 7) / 8), bx(256);
   const dim3 gs((unsigned)std::min<size_t>(ks_grid, BT)), gc((unsigned)std::min<size_t>(kc_grid, BT));
   void* kp = nh_stream_kernel(0);
   void* kx = nh_stream_kernel(1);

@@ -52,14 +52,23 @@ NH_DEV Side ghost_side(const Side& in, int bc) {
 
 // hydrostatic.py:131-160 with the general (reconstructed) formulas.  They are
 // bit-identical to the plain branch when dL == dR: hLs == hL,
-// corr == 0, (hLs/hL) == 1.
+// corr == 0, (hLs/hL) == 1.  LEVEL = true is that plain branch, used for
+// flat-bottom members where dL == dR at every face: the reconstruction terms
+// are exact zeros there (up to the sign of a zero flux, which no later
+// operation can observe), so they are skipped.
+template <bool LEVEL = false>
 NH_DEV Face face_flux(const Side& L, const Side& R, double g, double& speed) {
   const double hg = 0.5 * g;
-  double dm = fmin(L.d, R.d);
-  double hLs = fmax(RSUB(L.h, RSUB(L.d, dm)), 0.0);
-  double hRs = fmax(RSUB(R.h, RSUB(R.d, dm)), 0.0);
-  double cL = RMUL(hg, RSUB(RMUL(L.h, L.h), RMUL(hLs, hLs)));
-  double cR = RMUL(hg, RSUB(RMUL(R.h, R.h), RMUL(hRs, hRs)));
+  double hLs, hRs, cL = 0.0, cR = 0.0;
+  if (LEVEL) {
+    hLs = L.h; hRs = R.h;
+  } else {
+    double dm = fmin(L.d, R.d);
+    hLs = fmax(RSUB(L.h, RSUB(L.d, dm)), 0.0);
+    hRs = fmax(RSUB(R.h, RSUB(R.d, dm)), 0.0);
+    cL = RMUL(hg, RSUB(RMUL(L.h, L.h), RMUL(hLs, hLs)));
+    cR = RMUL(hg, RSUB(RMUL(R.h, R.h), RMUL(hRs, hRs)));
+  }
   double aL = RADD(fabs(L.u), RSQRT(RMUL(g, hLs)));
   double aR = RADD(fabs(R.u), RSQRT(RMUL(g, hRs)));
   speed = fmax(aL, aR);
@@ -69,23 +78,30 @@ NH_DEV Face face_flux(const Side& L, const Side& R, double g, double& speed) {
   f.F1 = RSUB(RMUL(0.5, RADD(qL, qR)), RMUL(lam, RSUB(hRs, hLs)));
   double s2 = RADD(RADD(RMUL(qL, L.u), RMUL(qR, R.u)), RMUL(hg, RADD(RMUL(hLs, hLs), RMUL(hRs, hRs))));
   double F2 = RSUB(RMUL(0.5, s2), RMUL(lam, RSUB(qR, qL)));
+  double wL, wR;
+  if (LEVEL) {
+    wL = L.hw; wR = R.hw;
+  } else {
 #if NH_STRICT
-  // (hLs / hL) hwL is exactly hwL when hLs == hL (IEEE x / x == 1)
-  double wL = (hLs == L.h) ? L.hw : RMUL(RDIVP(hLs, L.h), L.hw);
-  double wR = (hRs == R.h) ? R.hw : RMUL(RDIVP(hRs, R.h), R.hw);
+    // (hLs / hL) hwL is exactly hwL when hLs == hL (IEEE x / x == 1)
+    wL = (hLs == L.h) ? L.hw : RMUL(RDIVP(hLs, L.h), L.hw);
+    wR = (hRs == R.h) ? R.hw : RMUL(RDIVP(hRs, R.h), R.hw);
 #else
-  double wL = (hLs == L.h) ? L.hw : (hLs * L.rh) * L.hw;
-  double wR = (hRs == R.h) ? R.hw : (hRs * R.rh) * R.hw;
+    wL = (hLs == L.h) ? L.hw : (hLs * L.rh) * L.hw;
+    wR = (hRs == R.h) ? R.hw : (hRs * R.rh) * R.hw;
 #endif
+  }
   f.F3 = RSUB(RMUL(0.5, RADD(RMUL(wL, L.u), RMUL(wR, R.u))), RMUL(lam, RSUB(wR, wL)));
-  f.F2L = RADD(F2, cL);
-  f.F2R = RADD(F2, cR);
+  f.F2L = LEVEL ? F2 : RADD(F2, cL);
+  f.F2R = LEVEL ? F2 : RADD(F2, cR);
   return f;
 }
 
 // Tendency of one element (hydrostatic.py:162-183).  n0/n1 = own nodes,
-// fl = face at its left, fr = face at its right, dx0/dx1 = bottom slope.
+// fl = face at its left, fr = face at its right, dx0/dx1 = bottom slope
+// (LEVEL: identically zero, the g h d_x source is skipped).
 // The volume products keep numpy's dgemm rounding: fma(v1, W1, v0*W0).
+template <bool LEVEL = false>
 NH_DEV void element_tendency(const nh_member& m, double g, const Side& n0, const Side& n1,
                              const Face& fl, const Face& fr, double dx0, double dx1,
                              double t[6]) {
@@ -104,7 +120,7 @@ NH_DEV void element_tendency(const nh_member& m, double g, const Side& n0, const
     double v2 = fma(f21, W[2 * i + 1], RMUL(f20, W[2 * i]));
     v2 = RSUB(v2, RMUL(fr.F2L, lr[i]));
     v2 = RADD(v2, RMUL(fl.F2R, ll[i]));
-    t[2 + i] = RADD(v2, RMUL(RMUL(g, i ? n1.h : n0.h), i ? dx1 : dx0));
+    t[2 + i] = LEVEL ? v2 : RADD(v2, RMUL(RMUL(g, i ? n1.h : n0.h), i ? dx1 : dx0));
     double v3 = fma(f31, W[2 * i + 1], RMUL(f30, W[2 * i]));
     v3 = RSUB(v3, RMUL(fr.F3, lr[i]));
     t[4 + i] = RADD(v3, RMUL(fl.F3, ll[i]));

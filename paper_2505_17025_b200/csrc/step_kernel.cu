@@ -128,7 +128,7 @@ __device__ __forceinline__ double stage(const nh_member& m, double g, const doub
     SideX B0 = load_side<KIND>(m, bt, src, S, j0 + k, e0d + k, 0);
     SideX B1 = load_side<KIND>(m, bt, src, S, j0 + k, e0d + k, 1);
     Side L = (e0 + k == 0) ? ghost_side(B0.s, m.bc_left) : Lprev;
-    Face Fk = face_flux(L, B0.s, g, sp);
+    Face Fk = face_flux<KIND == NH_BOTTOM_FLAT>(L, B0.s, g, sp);
     speed = fmax(speed, sp);
     if (k == 0) {
       sm.Fx[0 * sm.T + tid] = Fk.F1;
@@ -137,11 +137,11 @@ __device__ __forceinline__ double stage(const nh_member& m, double g, const doub
     } else {
       Face Fr = Fk;
       if (e0 + k - 1 == N - 1) {
-        Fr = face_flux(P1.s, ghost_side(P1.s, m.bc_right), g, sp);
+        Fr = face_flux<KIND == NH_BOTTOM_FLAT>(P1.s, ghost_side(P1.s, m.bc_right), g, sp);
         speed = fmax(speed, sp);
       }
       Tend6 td;
-      element_tendency(m, g, P0.s, P1.s, PF, Fr, P0.sx, P1.sx, td.v);
+      element_tendency<KIND == NH_BOTTOM_FLAT>(m, g, P0.s, P1.s, PF, Fr, P0.sx, P1.sx, td.v);
       fn(k - 1, td);
     }
     P0 = B0; P1 = B1; PF = Fk; Lprev = B1.s;
@@ -150,7 +150,7 @@ __device__ __forceinline__ double stage(const nh_member& m, double g, const doub
   {
     Face fr;
     if (e0 + E - 1 == N - 1) {
-      fr = face_flux(P1.s, ghost_side(P1.s, m.bc_right), g, sp);
+      fr = face_flux<KIND == NH_BOTTOM_FLAT>(P1.s, ghost_side(P1.s, m.bc_right), g, sp);
       speed = fmax(speed, sp);
     } else {
       int tn = tid + 1 < sm.T ? tid + 1 : tid;
@@ -160,7 +160,7 @@ __device__ __forceinline__ double stage(const nh_member& m, double g, const doub
       fr.F2R = 0.0;
     }
     Tend6 td;
-    element_tendency(m, g, P0.s, P1.s, PF, fr, P0.sx, P1.sx, td.v);
+    element_tendency<KIND == NH_BOTTOM_FLAT>(m, g, P0.s, P1.s, PF, fr, P0.sx, P1.sx, td.v);
     fn(E - 1, td);
   }
   return speed;

@@ -98,7 +98,7 @@ __device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q
   if (e == 0) L = ghost_side(n0, m.bc_left);
   // (CTA slot 0 keeps lane 0's own value: a halo element, never used)
   double sp;
-  Face fl = face_flux(L, n0, g, sp);
+  Face fl = face_flux<KIND == NH_BOTTOM_FLAT>(L, n0, g, sp);
   speed = fmax(speed, sp);
   Face fr;
   fr.F1 = __shfl_down_sync(0xffffffffu, fl.F1, 1);
@@ -118,10 +118,10 @@ __device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q
     }
   }
   if (e == N - 1) {
-    fr = face_flux(n1, ghost_side(n1, m.bc_right), g, sp);
+    fr = face_flux<KIND == NH_BOTTOM_FLAT>(n1, ghost_side(n1, m.bc_right), g, sp);
     speed = fmax(speed, sp);
   }
-  element_tendency(m, g, n0, n1, fl, fr, b0.d_x, b1.d_x, t6);
+  element_tendency<KIND == NH_BOTTOM_FLAT>(m, g, n0, n1, fl, fr, b0.d_x, b1.d_x, t6);
   d0 = b0.d; d1 = b1.d;
 }
 #else
@@ -155,19 +155,19 @@ __device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q
 #endif
   }
   double sp;
-  Face fl = face_flux(L, n0, g, sp);
+  Face fl = face_flux<KIND == NH_BOTTOM_FLAT>(L, n0, g, sp);
   speed = fmax(speed, sp);
   sf[0 * TPB + i] = fl.F1; sf[1 * TPB + i] = fl.F2L; sf[2 * TPB + i] = fl.F3;
   __syncthreads();
   Face fr;
   if (e == N - 1) {
-    fr = face_flux(n1, ghost_side(n1, m.bc_right), g, sp);
+    fr = face_flux<KIND == NH_BOTTOM_FLAT>(n1, ghost_side(n1, m.bc_right), g, sp);
     speed = fmax(speed, sp);
   } else {
     int k = i < TPB - 1 ? i + 1 : i;
     fr.F1 = sf[0 * TPB + k]; fr.F2L = sf[1 * TPB + k]; fr.F3 = sf[2 * TPB + k]; fr.F2R = 0.0;
   }
-  element_tendency(m, g, n0, n1, fl, fr, b0.d_x, b1.d_x, t6);
+  element_tendency<KIND == NH_BOTTOM_FLAT>(m, g, n0, n1, fl, fr, b0.d_x, b1.d_x, t6);
   d0 = b0.d; d1 = b1.d;
 }
 
@@ -242,7 +242,8 @@ struct TileIdx {
 
 __device__ __forceinline__ TileIdx tile_idx(const StreamArgs& a) {
   TileIdx t;
-  t.b = blockIdx.x / a.tiles; t.tile = blockIdx.x % a.tiles;
+  // grid (tiles, members): no integer division (members past 65535 in z)
+  t.b = blockIdx.z * 65535 + blockIdx.y; t.tile = blockIdx.x;
   t.i = threadIdx.x; t.lane = t.i & 31; t.warp = t.i >> 5;
   t.e = t.tile * OWN - H + t.i;
   t.valid = t.e >= 0 && t.e < a.N;
@@ -318,7 +319,8 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   double speed = 0.0;
 
   // ---------------- Heun stage 1 at t ----------------
-  if (own && (q.h0 <= 0.0 || q.h1 <= 0.0)) nh_report(st, step, NH_ERR_POSITIVITY_ENTRY, e);
+  // positivity (hydrostatic.py:101-103, 216-217) gathered into one report
+  unsigned bad = (own && (q.h0 <= 0.0 || q.h1 <= 0.0)) ? 1u : 0u;
   ks.sq[0 * TPB + i] = q.h0; ks.sq[1 * TPB + i] = q.h1; ks.sq[2 * TPB + i] = q.q0;
   ks.sq[3 * TPB + i] = q.q1; ks.sq[4 * TPB + i] = q.w0; ks.sq[5 * TPB + i] = q.w1;
   Q6 qs;
@@ -331,7 +333,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
             RADD(q.q0, RMUL(dt, k1[2])), RADD(q.q1, RMUL(dt, k1[3])),
             RADD(q.w0, RMUL(dt, k1[4])), RADD(q.w1, RMUL(dt, k1[5]))};
   }
-  if (own && !(qs.h0 > 0.0 && qs.h1 > 0.0)) nh_report(st, step, NH_ERR_POSITIVITY_STAGE1, -1);
+  bad |= (own && !(qs.h0 > 0.0 && qs.h1 > 0.0)) ? 2u : 0u;
 #if !NH_KP_WARP_XCHG
   __syncthreads();   // every read of sh / sf of stage 1 is done
 #endif
@@ -347,7 +349,12 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   for (int f = 0; f < 6; ++f)
     qv[f] = RADD(ks.sq[f * TPB + i], RMUL(dt, RMUL(0.5, RADD(ks.sk[f * TPB + i], k2[f]))));
   Q6 qp{qv[0], qv[1], qv[2], qv[3], qv[4], qv[5]};
-  if (own && !(qp.h0 > 0.0 && qp.h1 > 0.0)) nh_report(st, step, NH_ERR_POSITIVITY_STAGE2, -1);
+  bad |= (own && !(qp.h0 > 0.0 && qp.h1 > 0.0)) ? 4u : 0u;
+  if (bad)   // the reference raises at the first failing check: lowest code wins
+    nh_report(st, step,
+              (bad & 1u) ? NH_ERR_POSITIVITY_ENTRY
+                         : ((bad & 2u) ? NH_ERR_POSITIVITY_STAGE1 : NH_ERR_POSITIVITY_STAGE2),
+              (bad & 1u) ? e : -1);
   if (own) {
     *reinterpret_cast<double2*>(a.h_out + o) = double2{qp.h0, qp.h1};
     *reinterpret_cast<double2*>(a.hu_out + o) = double2{qp.q0, qp.q1};
@@ -443,7 +450,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
       if (nf == 0) store_super(ta, super_gap(qp.q0));
       if (nf) {
         atomicAdd((unsigned long long*)&st->flagged, (unsigned long long)nf);
-        a.tile_list[atomicAdd(a.tile_count, 1)] = blockIdx.x;   // work list of K_S / K_C
+        a.tile_list[atomicAdd(a.tile_count, 1)] = b * T + tile;   // work list of K_S / K_C
       }
     }
     // right-end ghost outer trace (corrector.py:400-402)
@@ -536,6 +543,7 @@ __global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(Stream
   __shared__ MemberConst mc;
   __shared__ KpSmem ks;
   const TileIdx ti = tile_idx(a);
+  if (ti.b >= a.B) return;   // padding of the (tiles, 65535, z) grid
   const int N = a.N, i = ti.i, b = ti.b, e = ti.e;
 
   // state and the previous step's pending record are requested first so their
