@@ -194,6 +194,50 @@ class QuarticSlide(Bottom):
                 np.where(inside, Hs * 12.0 * xi ** 2 * c * c, 0.0))
 
 
+# Deterministic elementary functions of the harness models.  The two harness
+# bottoms (configs 2-5) are this project's own closed forms (SURVEY.md
+# Appendix C), so they are DEFINED through exp / log1p evaluated with IEEE
+# +, -, * and / only (Cody-Waite reduction, Horner polynomials, no fused
+# multiply-add), which numpy on any host and the CUDA kernels (bathy.cuh
+# nh_det_exp / nh_det_log1p, same constants, same order) round identically.
+# libm / numpy-SIMD / CUDA exp differ from each other in the last bit, and a
+# per-step last-bit difference in d(x, t) random-walks through the predictor.
+LN2_HI = float.fromhex("0x1.62e42fee00000p-1")     # k * LN2_HI exact for |k| < 2^11
+LN2_LO = float.fromhex("0x1.a39ef35793c76p-33")
+INV_LN2 = float.fromhex("0x1.71547652b82fep+0")
+LN2 = math.log(2.0)
+_EXP_TAYLOR = [1.0 / math.factorial(n) for n in range(13, -1, -1)]   # 1/13!, ..., 1/0!
+_ATANH_ODD = [1.0 / (2 * k + 1) for k in range(17, -1, -1)]          # 1/35, ..., 1/1
+BOX_YCUT = 23.0      # smoothed box: S(x) = 0 beyond |y| = 23 (E < 1e-20)
+SLIDE_RCUT = 10.0    # Gaussian mound: G = 0 beyond |r| = 10 (< 2e-22 A)
+
+
+def det_exp(x):
+    """exp(x) from IEEE +,-,* only: x = k ln2 + r, |r| <= ln2/2, degree-13
+    Taylor polynomial of exp(r) by Horner, times 2^k."""
+    x = np.asarray(x, dtype=np.float64)
+    k = np.rint(x * INV_LN2)
+    r = (x - k * LN2_HI) - k * LN2_LO
+    p = np.full_like(r, _EXP_TAYLOR[0])
+    for c in _EXP_TAYLOR[1:]:
+        p = p * r + c
+    out = np.ldexp(p, k.astype(np.int64))
+    return out if out.ndim else float(out)
+
+
+def det_log1p(e):
+    """log1p(e) for 0 <= e <= 1 as 2 atanh(z), z = e / (2 + e) <= 1/3: odd
+    series to z^35 by Horner in z^2."""
+    e = np.asarray(e, dtype=np.float64)
+    z = e / (2.0 + e)
+    w = z * z
+    s = np.full_like(z, _ATANH_ODD[0])
+    for c in _ATANH_ODD[1:]:
+        s = s * w + c
+    out = 2.0 * (z * s)
+    return out if out.ndim else float(out)
+
+
 @dataclass
 class SmoothBox(Bottom):
     """Harness model (configs 2, 4): box uplift with a tanh edge.
@@ -202,8 +246,9 @@ class SmoothBox(Bottom):
     S = (1 - tanh((|x| - b)/w)) / 2, written through E = exp(-2|y|),
     y = (|x| - b)/w, so that no channel suffers cancellation:
     S = E/(1+E) (y >= 0) or 1/(1+E) (y < 0); S' = -2E/(1+E)^2 sign(x)/w;
-    S'' = 4E(1-E)/(1+E)^3 sign(y)/w^2.  Shared with the CUDA device model
-    (csrc/bathy.cuh) -- SURVEY.md Appendix C.3.
+    S'' = 4E(1-E)/(1+E)^3 sign(y)/w^2; S = S' = S'' = 0 for y >= 23.
+    exp is det_exp.  Shared with the CUDA device model (csrc/bathy.cuh) --
+    SURVEY.md Appendix C.3.
     """
     h0: float
     zeta0: float
@@ -213,13 +258,14 @@ class SmoothBox(Bottom):
 
     def channels(self, x, t):
         tt = max(t, 0.0)
-        e = math.exp(-self.alpha * tt)
+        e = det_exp(-self.alpha * tt)
         zeta = self.zeta0 * (1.0 - e)
         zt = self.zeta0 * self.alpha * e
         ztt = -self.zeta0 * self.alpha * self.alpha * e
         ax = np.abs(x)
         y = (ax - self.b) / self.w
-        E = np.exp(-2.0 * np.abs(y))
+        on = y < BOX_YCUT
+        E = np.where(on, det_exp(-2.0 * np.abs(np.where(on, y, 0.0))), 0.0)
         inv1 = 1.0 / (1.0 + E)
         S = np.where(y >= 0.0, E * inv1, inv1)
         sg = np.where(x >= 0.0, 1.0, -1.0)
@@ -234,11 +280,13 @@ class SmoothBox(Bottom):
 class SlopeSlide(Bottom):
     """Harness model (configs 3, 5): Gaussian mound sliding down a plane slope.
 
-    d0(x) = min(d_top + x tan(theta), d_max);  G = A exp(-((x-xc)/sigma)^2 / 2);
-    d = d0 - G.  xc(t) = x0 + u_t t0 ln cosh(t/t0) until d0(xc) = d_stop, then
-    frozen (velocity u_t tanh(t/t0), acceleration (u_t/t0) sech^2(t/t0)).
-    d_t = G_x xc', d_tt = -G_xx xc'^2 + G_x xc'', d_xt = G_xx xc', d_xx = -G_xx
-    (the slope kink's d0'' is taken as 0).  SURVEY.md Appendix C.4.
+    d0(x) = min(d_top + x tan(theta), d_max);  G = A exp(-((x-xc)/sigma)^2 / 2)
+    (0 beyond |x - xc| = 10 sigma);  d = d0 - G.  xc(t) = x0 + u_t t0 ln cosh(t/t0)
+    until d0(xc) = d_stop, then frozen (velocity u_t tanh(t/t0), acceleration
+    (u_t/t0) sech^2(t/t0)); ln cosh s = s + log1p(E) - ln 2 and
+    tanh s = (1 - E)/(1 + E) with E = exp(-2s); exp / log1p are det_exp /
+    det_log1p.  d_t = G_x xc', d_tt = -G_xx xc'^2 + G_x xc'', d_xt = G_xx xc',
+    d_xx = -G_xx (the slope kink's d0'' is taken as 0).  SURVEY.md Appendix C.4.
     """
     d_top: float
     tan_theta: float
@@ -268,8 +316,9 @@ class SlopeSlide(Bottom):
         if tt >= ts:
             return self.x_stop if ts > 0.0 else self.x0, 0.0, 0.0
         s = tt / self.t0
-        lc = s + math.log1p(math.exp(-2.0 * s)) - math.log(2.0)   # ln cosh(s)
-        th = math.tanh(s)
+        E = det_exp(-2.0 * s)
+        lc = s + det_log1p(E) - LN2                # ln cosh(s)
+        th = (1.0 - E) / (1.0 + E)                 # tanh(s)
         return (self.x0 + self.u_t * self.t0 * lc, self.u_t * th,
                 (self.u_t / self.t0) * (1.0 - th * th))
 
@@ -280,7 +329,8 @@ class SlopeSlide(Bottom):
         d0 = np.where(on_slope, ramp, self.d_max)
         d0x = np.where(on_slope, self.tan_theta, 0.0)
         r = (x - xc) / self.sigma
-        G = self.A * np.exp(-0.5 * r * r)
+        on = np.abs(r) < SLIDE_RCUT
+        G = np.where(on, self.A * det_exp(-0.5 * r * r), 0.0)
         Gx = -G * r / self.sigma
         Gxx = G * (r * r - 1.0) / (self.sigma * self.sigma)
         return (d0 - G, d0x - Gx, Gx * v, -Gxx * v * v + Gx * acc, Gxx * v, -Gxx)

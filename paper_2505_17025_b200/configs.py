@@ -278,19 +278,15 @@ class Config5(Config):
 
     def records(self, idx=None):
         from ._device import member_record
-        tab = self.table() if idx is None else self.table()[np.asarray(idx)]
+        idx = range(self.n_members) if idx is None else idx
         base = member_record(self.grid, FlatBottom(1.0), BoundaryPair(WALL, ABSORBING), self.dt)
-        rec = np.repeat(base, tab.shape[0])
-        tan_t, A, sigma, x0, u_t = tab.T
-        x_stop = 0.7 / tan_t
-        arg = (x_stop - x0) / (u_t * 0.5)
-        t_stop = np.where(arg > 0.0,
-                          0.5 * (arg + np.log1p(np.sqrt(-np.expm1(-2.0 * np.maximum(arg, 0.0))))),
-                          0.0)
+        rec = np.repeat(base, len(idx))
         rec["bottom_kind"] = _lib.BOTTOM_SLOPE_SLIDE
-        rec["bottom"][:, :12] = np.stack([np.full_like(tan_t, 0.1), tan_t, np.full_like(tan_t, 1.0),
-                                          A, sigma, x0, u_t, np.full_like(tan_t, 0.5),
-                                          np.full_like(tan_t, 0.8), x_stop, t_stop, 1.0 / sigma], 1)
+        # the bottom model's own pack(): x_stop / t_stop bit-identical to the
+        # model the oracle evaluates
+        for k, i in enumerate(idx):
+            _, params = self.member(int(i)).bathymetry.pack()
+            rec["bottom"][k, :len(params)] = params
         return rec
 
 

@@ -9,10 +9,10 @@
 // Every function is templated on the model kind so the step kernel runs a
 // straight-line path per member (KIND = -1 dispatches at run time).  Time
 // factors are hoisted into BottomTime once per instant.  The two harness
-// models skip their exp() where it is below 1e-20 (|y| > 23 for the tanh
-// box, |r| > 10 for the Gaussian): there the exact channels differ from the
-// flat/plane values by less than 1e-20 relative, far below the last bit of
-// d, so the cut is invisible at the parity tolerance.
+// models are defined (here and in the oracle) with a cut-off -- S = 0 for
+// |y| >= 23 (tanh box), G = 0 for |r| >= 10 (Gaussian) -- and with the
+// deterministic exp / log1p below, so device and host evaluate them to the
+// same bits.
 #pragma once
 #include "nh_common.cuh"
 
@@ -33,6 +33,33 @@ struct BottomTime {
 
 #define NH_BOX_YCUT 23.0
 #define NH_SLIDE_RCUT 10.0
+
+// Deterministic exp / log1p of the harness bottom models (oracle det_exp /
+// det_log1p): IEEE +,-,* only -- Cody-Waite reduction and Horner polynomials,
+// explicit round-to-nearest intrinsics (never contracted), same constants and
+// order as the numpy definition, so host and device round identically.
+__device__ __forceinline__ double nh_det_exp(double x) {
+  const double k = rint(__dmul_rn(x, 1.4426950408889634));
+  const double r = __dsub_rn(__dsub_rn(x, __dmul_rn(k, 0.6931471803691238)),
+                             __dmul_rn(k, 1.9082149292705877e-10));
+  const double c[14] = {1.6059043836821613e-10, 2.08767569878681e-09, 2.505210838544172e-08,
+                        2.755731922398589e-07,  2.7557319223985893e-06, 2.48015873015873e-05,
+                        0.0001984126984126984,  0.001388888888888889, 0.008333333333333333,
+                        0.041666666666666664,   0.16666666666666666, 0.5, 1.0, 1.0};
+  double p = c[0];
+#pragma unroll
+  for (int n = 1; n < 14; ++n) p = __dadd_rn(__dmul_rn(p, r), c[n]);
+  return scalbn(p, (int)k);
+}
+
+__device__ __forceinline__ double nh_det_log1p(double e) {
+  const double z = __ddiv_rn(e, __dadd_rn(2.0, e));
+  const double w = __dmul_rn(z, z);
+  double s = 1.0 / 35.0;
+#pragma unroll
+  for (int k = 16; k >= 0; --k) s = __dadd_rn(__dmul_rn(s, w), 1.0 / (2 * k + 1));
+  return __dmul_rn(2.0, __dmul_rn(z, s));
+}
 
 // sample coordinate of node j of an element whose index (as a double) is ed,
 // bit-identical to GridSpec: edges = x_left + dx*e ; node1 = edges + dx ;
@@ -68,8 +95,10 @@ template <int KIND>
 __device__ __forceinline__ BottomTime bottom_time_k(const nh_member& m, double t) {
   BottomTime bt{0.0, 0.0, 0.0};
   const double* p = m.bottom;
-  if (KIND == NH_BOTTOM_PLATE || KIND == NH_BOTTOM_SMOOTH_BOX) {
+  if (KIND == NH_BOTTOM_PLATE) {
     bt.a = exp(-p[3] * fmax(t, 0.0));
+  } else if (KIND == NH_BOTTOM_SMOOTH_BOX) {
+    bt.a = nh_det_exp(__dmul_rn(-p[3], fmax(t, 0.0)));
   } else if (KIND == NH_BOTTOM_QUARTIC_SLIDE) {
     double s, sp, spp;
     motion_at(p, t, s, sp, spp);
@@ -79,12 +108,13 @@ __device__ __forceinline__ BottomTime bottom_time_k(const nh_member& m, double t
     if (tt >= ts) {
       bt.a = ts > 0.0 ? p[9] : p[5];
     } else {
-      double s = tt / p[7];
-      double lc = s + log1p(exp(-2.0 * s)) - 0.6931471805599453;  // ln cosh(s)
-      double th = tanh(s);
-      bt.a = p[5] + p[6] * p[7] * lc;
-      bt.b = p[6] * th;
-      bt.c = (p[6] / p[7]) * (1.0 - th * th);
+      const double s = __ddiv_rn(tt, p[7]);
+      const double E = nh_det_exp(__dmul_rn(-2.0, s));
+      const double lc = __dsub_rn(__dadd_rn(s, nh_det_log1p(E)), 0.6931471805599453);  // ln cosh
+      const double th = __ddiv_rn(__dsub_rn(1.0, E), __dadd_rn(1.0, E));               // tanh
+      bt.a = __dadd_rn(p[5], __dmul_rn(__dmul_rn(p[6], p[7]), lc));
+      bt.b = __dmul_rn(p[6], th);
+      bt.c = __dmul_rn(__ddiv_rn(p[6], p[7]), __dsub_rn(1.0, __dmul_rn(th, th)));
     }
   }
   return bt;
@@ -141,7 +171,7 @@ __device__ __forceinline__ Bottom6 bottom_eval(const nh_member& m, const BottomT
     if (y < NH_BOX_YCUT) {
       double decay = bt.a, z0 = p[1], al = p[3];
       double zeta = RMUL(z0, RSUB(1.0, decay));
-      double E = exp(RMUL(-2.0, fabs(y)));
+      double E = nh_det_exp(RMUL(-2.0, fabs(y)));
       double inv1 = RDIV(1.0, RADD(1.0, E));
       double S = y >= 0.0 ? RMUL(E, inv1) : inv1;
       double sg = x >= 0.0 ? 1.0 : -1.0;
@@ -167,7 +197,7 @@ __device__ __forceinline__ Bottom6 bottom_eval(const nh_member& m, const BottomT
     b.d_x = on ? p[1] : 0.0;
     double r = RDIV(RSUB(x, bt.a), p[4]);
     if (fabs(r) < NH_SLIDE_RCUT) {
-      double G = RMUL(p[3], exp(RMUL(RMUL(-0.5, r), r)));
+      double G = RMUL(p[3], nh_det_exp(RMUL(RMUL(-0.5, r), r)));
       double Gx = RDIV(RMUL(-G, r), p[4]);
       b.d = RSUB(b.d, G);
       b.d_x = RSUB(b.d_x, Gx);
@@ -199,7 +229,7 @@ __device__ __forceinline__ BottomSpace bottom_space(const nh_member& m, double x
     const double* p = m.bottom;
     double y = RDIV(RSUB(fabs(x), p[2]), p[4]);
     if (y < NH_BOX_YCUT) {
-      double E = exp(RMUL(-2.0, fabs(y)));
+      double E = nh_det_exp(RMUL(-2.0, fabs(y)));
       double inv1 = RDIV(1.0, RADD(1.0, E));
       sp.S = y >= 0.0 ? RMUL(E, inv1) : inv1;
       double sg = x >= 0.0 ? 1.0 : -1.0;

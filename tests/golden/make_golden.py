@@ -160,6 +160,9 @@ def digest(flags: np.ndarray) -> int:
     return zlib.crc32(np.packbits(flags).tobytes())
 
 
+CHECKPOINTS = {"config3": (500, 5000, 10000, 15000, 20000, 25000, 30000)}
+
+
 def long_fixture(name, n_steps=None):
     from paper_2505_17025_b200 import configs
     from tests.helpers import oracle_depth
@@ -183,22 +186,34 @@ def long_fixture(name, n_steps=None):
     assert spec.n_steps == steps
     init = R.FlowState(R.NodalField(grid, h), R.NodalField(grid, hu), R.NodalField(grid, hw), 0.0)
     data = {"h0": h, "hu0": hu, "hw0": hw, "dt": np.array(m.dt), "n_steps": np.array(steps)}
+    ck = set(CHECKPOINTS.get(name, ()))
     for mode in cfg.modes:
         crit = R.Criterion("eta_over_d") if mode == "adaptive" else None
         t0 = time.time()
-        res = R.simulate(spec, init, mode, crit, record_masks=True)
-        fs = res.final_state
-        data[mode + "/final"] = np.stack([fs.h.values, fs.hu.values, fs.hw.values])
-        data[mode + "/loop_time"] = np.array(res.loop_time)
-        data[mode + "/mask_fraction"] = np.array(res.mask_fraction_mean)
-        if mode == "adaptive":
-            cnt, dig = [], []
-            for _, _, ranges in res.mask_history:
+        # driver.simulate's loop (driver.py:79-94), unrolled here so the
+        # reference state can also be saved at checkpoint steps
+        state, loop_time, fractions, cnt, dig = init, 0.0, [], [], []
+        for step in range(steps):
+            s0 = time.perf_counter()
+            res = R.adaptive_step(state, spec.dt, spec.bathymetry, spec.bcs, mode=mode, crit=crit,
+                                  g=spec.g)
+            loop_time += time.perf_counter() - s0
+            state = res.state
+            fractions.append(res.mask.fraction)
+            if mode == "adaptive":
                 f = np.zeros(grid.n_elements, bool)
-                for e0, e1 in ranges:
+                for e0, e1 in res.mask.ranges:
                     f[e0:e1 + 1] = True
                 cnt.append(int(f.sum()))
                 dig.append(digest(f))
+            if mode == "adaptive" and step + 1 in ck:
+                data[f"ck/s{step + 1}"] = np.stack([state.h.values, state.hu.values, state.hw.values])
+                data[f"ck/t{step + 1}"] = np.array(state.time)
+        fs = state
+        data[mode + "/final"] = np.stack([fs.h.values, fs.hu.values, fs.hw.values])
+        data[mode + "/loop_time"] = np.array(loop_time)
+        data[mode + "/mask_fraction"] = np.array(float(np.mean(fractions)))
+        if mode == "adaptive":
             data[mode + "/flag_count"] = np.array(cnt, dtype=np.int32)
             data[mode + "/flag_crc"] = np.array(dig, dtype=np.uint32)
         print(f"{name} {mode}: {steps} steps in {time.time() - t0:.1f}s", flush=True)

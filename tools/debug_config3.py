@@ -1,4 +1,4 @@
-"""Config 3 on the GPU vs oracle checkpoints (tests/golden/config3_checkpoints.npz)."""
+"""Config 3 on the GPU vs the reference checkpoints (tests/golden/config3_full.npz ck/*)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -6,13 +6,13 @@ import paper_2505_17025_b200 as P
 from paper_2505_17025_b200 import configs
 from oracle import nhswe_oracle as O
 from tests.helpers import oracle_member, oracle_depth
-C = np.load('tests/golden/config3_checkpoints.npz')
 G = np.load('tests/golden/config3_full.npz')
+C = {k[3:]: G[k] for k in G.files if k.startswith('ck/')}
 cfg = configs.config3(); m = cfg.member(0)
 ens = P.Ensemble.from_host(cfg.records(), G['h0'][None], G['hu0'][None], G['hw0'][None])
 done = 0
 rel = lambda a, b: np.abs(a - b).max() / np.abs(b).max()
-for c in sorted(int(k[1:]) for k in C.files if k.startswith('s')):
+for c in sorted(int(k[1:]) for k in C if k.startswith('s')):
     ens.advance(c - done, "adaptive", P.Criterion("eta_over_d"), path=sys.argv[1] if len(sys.argv) > 1 else "auto")
     done = c
     ens.check()
