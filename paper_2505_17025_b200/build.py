@@ -17,9 +17,9 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libnhswe_b200.so")
-SOURCES = ["capi.cu", "step_kernel.cu", "aux_kernels.cu", "stream_kernels.cu"]
+SOURCES = ["capi.cu", "step_kernel.cu", "aux_kernels.cu", "stream_kernels.cu", "stream_kp.cu"]
 HEADERS = ["nh_common.cuh", "bathy.cuh", "physics.cuh", "tree.cuh", "step_kernel.cuh",
-           "stream_kernels.cuh"]
+           "stream_kernels.cuh", "stream_kp.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "--extended-lambda", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 # default build: reference-faithful arithmetic (NH_STRICT=1, no implicit FMA contraction);
@@ -50,18 +50,21 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     if not force and out is None and not _stale():
         return LIB
     os.makedirs(os.path.dirname(lib), exist_ok=True)
-    objs = []
-    for src in SOURCES:
+    objs, procs = [], []
+    for src in SOURCES:   # one nvcc per source, concurrently
         obj = os.path.join(os.path.dirname(lib), src.replace(".cu", ".o"))
         cmd = [_nvcc(), *NVCC_FLAGS, *(FAST_FLAGS if fast else STRICT_FLAGS),
                *[f"-D{d}" for d in defines], "-c",
                os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}\n{r.stderr}")
-        if verbose:
-            sys.stderr.write(r.stderr)
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                            text=True)))
         objs.append(obj)
+    for src, p in procs:
+        out, err = p.communicate()
+        if p.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}:\n{out}\n{err}")
+        if verbose:
+            sys.stderr.write(err)
     tmp = lib + ".tmp"
     cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
            *objs, "-o", tmp]

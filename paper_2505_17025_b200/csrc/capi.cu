@@ -276,7 +276,7 @@ static int stream_tiles(int n) { return (n + NH_STREAM_OWN - 1) / NH_STREAM_OWN;
 size_t nh_stream_workspace_bytes(int n_members, int n_elements) {
   size_t BN = (size_t)n_members * n_elements, BT = (size_t)n_members * stream_tiles(n_elements);
   size_t dbl = 6 * BN + 12 * BN + 12 * BN + 10 * BT + 16 * (size_t)n_members;
-  return dbl * 8 + 2 * BN + 4 * (size_t)n_members + 8 + 4 * BT + 1024;
+  return dbl * 8 + 2 * BN + 4 * (size_t)n_members + 8 + 4 * BT + 4 * (size_t)n_members + 1024;
 }
 
 int nh_stream_advance(const nh_member* members, int B, int N, double* h, double* hu, double* hw,
@@ -307,6 +307,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   int* counter = (int*)(((uintptr_t)w + 15) & ~(uintptr_t)15);
   int* tcount = counter + B;            // [2] flagged-tile counters (ping-pong by step)
   int* tlist = tcount + 2;              // [B*T] flagged-tile list
+  int* order = tlist + BT;              // [B] K_P member order (by bottom kind)
   if (cudaMemsetAsync(counter, 0, 4 * ((size_t)B + 2), s) != cudaSuccess) return NH_E_CUDA;
   static int ks_grid = 0, kc_grid = 0;   // persistent grids: resident CTAs x SMs
   if (!ks_grid) {
@@ -331,6 +332,8 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   a.flag_bits = outputs ? outputs->flag_bits : nullptr;
   a.sch = sc; a.B = B; a.N = N; a.tiles = T; a.finalize = 0;
   a.tile_list = tlist; a.mconst = mconst;
+  static const bool use_order = !getenv("NH_STREAM_ORDER") || atoi(getenv("NH_STREAM_ORDER")) != 0;
+  a.order = use_order ? order : nullptr;
   const dim3 gp(T, std::min(B, 65535), (B + 65534) / 65535), bp(NH_STREAM_THREADS),
       gx((B + 7) / 8), bx(256);
   const dim3 gs((unsigned)std::min<size_t>(ks_grid, BT)), gc((unsigned)std::min<size_t>(kc_grid, BT));
@@ -343,6 +346,8 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
     void* args[1] = {&a};
     if (int rc = stream_launch(nh_stream_kernel(4), 5, dim3((B + 255) / 256), dim3(256), args, s))
       return rc;
+    if (a.order)
+      if (int rc = stream_launch(nh_stream_kernel(5), 5, dim3(1), dim3(1024), args, s)) return rc;
   }
   int cur = 0;   // 0: state in A, 1: state in Bb
   for (int k = 0; k < n_steps; ++k) {

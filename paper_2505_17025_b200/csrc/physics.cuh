@@ -44,6 +44,24 @@ NH_DEV Side make_side(double h, double hu, double hw, double d) {
   return s;
 }
 
+// Both nodes of an element with the whole warp converged: the two divisions
+// take their fast path and one warp vote decides whether to redo them with
+// the complete IEEE sequence (bit-identical to make_side either way).
+NH_DEV void make_sides_warp(double h0, double hu0, double hw0, double d0, double h1, double hu1,
+                            double hw1, double d1, Side& n0, Side& n1) {
+#if NH_STRICT
+  n0.h = h0; n0.hu = hu0; n0.hw = hw0; n0.d = d0; n0.rh = 0.0;
+  n1.h = h1; n1.hu = hu1; n1.hw = hw1; n1.d = d1; n1.rh = 0.0;
+  bool bad = false;
+  n0.u = nh_div_pos_fp(hu0, h0, bad);
+  n1.u = nh_div_pos_fp(hu1, h1, bad);
+  NH_WARP_FIX(bad, (n0.u = RDIVP(hu0, h0), n1.u = RDIVP(hu1, h1)));
+#else
+  n0 = make_side(h0, hu0, hw0, d0);
+  n1 = make_side(h1, hu1, hw1, d1);
+#endif
+}
+
 NH_DEV Side ghost_side(const Side& in, int bc) {
   Side s = in;
   if (bc == NH_BC_WALL) { s.hu = -in.hu; s.u = -in.u; }
@@ -56,7 +74,9 @@ NH_DEV Side ghost_side(const Side& in, int bc) {
 // flat-bottom members where dL == dR at every face: the reconstruction terms
 // are exact zeros there (up to the sign of a zero flux, which no later
 // operation can observe), so they are skipped.
-template <bool LEVEL = false>
+// WARP = true: every lane of the warp calls this together (one vote per
+// group of divisions / square roots instead of a branch per operation).
+template <bool LEVEL = false, bool WARP = false>
 NH_DEV Face face_flux(const Side& L, const Side& R, double g, double& speed) {
   const double hg = 0.5 * g;
   double hLs, hRs, cL = 0.0, cR = 0.0;
@@ -69,8 +89,21 @@ NH_DEV Face face_flux(const Side& L, const Side& R, double g, double& speed) {
     cL = RMUL(hg, RSUB(RMUL(L.h, L.h), RMUL(hLs, hLs)));
     cR = RMUL(hg, RSUB(RMUL(R.h, R.h), RMUL(hRs, hRs)));
   }
-  double aL = RADD(fabs(L.u), RSQRT(RMUL(g, hLs)));
-  double aR = RADD(fabs(R.u), RSQRT(RMUL(g, hRs)));
+  double sL, sR;
+#if NH_STRICT
+  if (WARP) {
+    bool bad = false;
+    sL = nh_dsqrt_rn_fp(RMUL(g, hLs), bad);
+    sR = nh_dsqrt_rn_fp(RMUL(g, hRs), bad);
+    NH_WARP_FIX(bad, (sL = RSQRT(RMUL(g, hLs)), sR = RSQRT(RMUL(g, hRs))));
+  } else
+#endif
+  {
+    sL = RSQRT(RMUL(g, hLs));
+    sR = RSQRT(RMUL(g, hRs));
+  }
+  double aL = RADD(fabs(L.u), sL);
+  double aR = RADD(fabs(R.u), sR);
   speed = fmax(aL, aR);
   double lam = RMUL(0.5, speed);
   double qL = RMUL(hLs, L.u), qR = RMUL(hRs, R.u);
@@ -84,8 +117,20 @@ NH_DEV Face face_flux(const Side& L, const Side& R, double g, double& speed) {
   } else {
 #if NH_STRICT
     // (hLs / hL) hwL is exactly hwL when hLs == hL (IEEE x / x == 1)
-    wL = (hLs == L.h) ? L.hw : RMUL(RDIVP(hLs, L.h), L.hw);
-    wR = (hRs == R.h) ? R.hw : RMUL(RDIVP(hRs, R.h), R.hw);
+    if (WARP) {
+      wL = L.hw; wR = R.hw;
+      const bool nL = hLs != L.h, nR = hRs != R.h;
+      if (__any_sync(0xffffffffu, nL || nR)) {
+        bool bad = false;
+        double rL = nh_div_pos_fp(hLs, L.h, bad), rR = nh_div_pos_fp(hRs, R.h, bad);
+        NH_WARP_FIX(bad, (rL = RDIVP(hLs, L.h), rR = RDIVP(hRs, R.h)));
+        if (nL) wL = RMUL(rL, L.hw);
+        if (nR) wR = RMUL(rR, R.hw);
+      }
+    } else {
+      wL = (hLs == L.h) ? L.hw : RMUL(RDIVP(hLs, L.h), L.hw);
+      wR = (hRs == R.h) ? R.hw : RMUL(RDIVP(hRs, R.h), R.hw);
+    }
 #else
     wL = (hLs == L.h) ? L.hw : (hLs * L.rh) * L.hw;
     wR = (hRs == R.h) ? R.hw : (hRs * R.rh) * R.hw;

@@ -105,7 +105,9 @@ __device__ __forceinline__ SideX load_side(const nh_member& m, const BottomTime&
 template <int E, int KIND, class Fn>
 __device__ __forceinline__ double stage(const nh_member& m, double g, const double* src,
                                         const Smem& sm, int tid, int j0, int e0, double e0d,
-                                        int N, const BottomTime& bt, Fn fn) {
+                                        int N, int c0, int c1, const BottomTime& bt, Fn fn) {
+  // speed: max over the left faces of own elements [c0, c1) and the right
+  // ghost face (halo slots past the domain ends hold no state)
   const int S = sm.S;
   double speed = 0.0, sp;
   // carried state: the previous slot's two nodes and its left face
@@ -129,7 +131,7 @@ __device__ __forceinline__ double stage(const nh_member& m, double g, const doub
     SideX B1 = load_side<KIND>(m, bt, src, S, j0 + k, e0d + k, 1);
     Side L = (e0 + k == 0) ? ghost_side(B0.s, m.bc_left) : Lprev;
     Face Fk = face_flux<KIND == NH_BOTTOM_FLAT>(L, B0.s, g, sp);
-    speed = fmax(speed, sp);
+    if (e0 + k >= c0 && e0 + k < c1) speed = fmax(speed, sp);
     if (k == 0) {
       sm.Fx[0 * sm.T + tid] = Fk.F1;
       sm.Fx[1 * sm.T + tid] = Fk.F2L;
@@ -138,7 +140,7 @@ __device__ __forceinline__ double stage(const nh_member& m, double g, const doub
       Face Fr = Fk;
       if (e0 + k - 1 == N - 1) {
         Fr = face_flux<KIND == NH_BOTTOM_FLAT>(P1.s, ghost_side(P1.s, m.bc_right), g, sp);
-        speed = fmax(speed, sp);
+        if (N - 1 >= c0 && N - 1 < c1) speed = fmax(speed, sp);
       }
       Tend6 td;
       element_tendency<KIND == NH_BOTTOM_FLAT>(m, g, P0.s, P1.s, PF, Fr, P0.sx, P1.sx, td.v);
@@ -151,7 +153,7 @@ __device__ __forceinline__ double stage(const nh_member& m, double g, const doub
     Face fr;
     if (e0 + E - 1 == N - 1) {
       fr = face_flux<KIND == NH_BOTTOM_FLAT>(P1.s, ghost_side(P1.s, m.bc_right), g, sp);
-      speed = fmax(speed, sp);
+      if (N - 1 >= c0 && N - 1 < c1) speed = fmax(speed, sp);
     } else {
       int tn = tid + 1 < sm.T ? tid + 1 : tid;
       fr.F1 = sm.Fx[0 * sm.T + tn];
@@ -222,7 +224,7 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
 
     if (do_pred) {
       // ---------------- stage 1 at t: Qs = Q* = Qn + dt k1, k1 parked in SK ----------------
-      double sp = stage<E, KIND>(m, g, sm.Qn, sm, tid, j0, e0, e0d, N, bt0,
+      double sp = stage<E, KIND>(m, g, sm.Qn, sm, tid, j0, e0, e0d, N, c0, c1, bt0,
                                  [&](int k, const Tend6 K1) {
         const double* k1 = K1.v;
         int j = j0 + k, e = e0 + k;
@@ -241,7 +243,7 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
       __syncthreads();
       NH_TS(0);
       // ---------------- stage 2 at t + dt: Qn = Qn + dt (k1 + k2)/2 (hydrostatic.py:208-209)
-      stage<E, KIND>(m, g, sm.Qs, sm, tid, j0, e0, e0d, N, bt1, [&](int k, const Tend6 K2) {
+      stage<E, KIND>(m, g, sm.Qs, sm, tid, j0, e0, e0d, N, c0, c1, bt1, [&](int k, const Tend6 K2) {
         const double* k2 = K2.v;
         int j = j0 + k, e = e0 + k;
 #pragma unroll

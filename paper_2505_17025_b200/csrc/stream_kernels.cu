@@ -22,209 +22,7 @@
 // The three launches of a step and the ping-pong of buffers are captured in
 // a CUDA graph by the host (stream.py).  A final K_P in "finalize" mode
 // applies the last pending hw update in place.
-#include <cooperative_groups.h>
-#include "bathy.cuh"
-#include "physics.cuh"
-#include "stream_kernels.cuh"
-#include "tree.cuh"
-
-namespace {
-
-constexpr int TPB = NH_STREAM_THREADS;     // 256
-constexpr int H = NH_STREAM_HALO;          // 4
-constexpr int OWN = TPB - 2 * H;           // 248
-constexpr int NW = TPB / 32;
-
-__device__ __forceinline__ double ederiv(const nh_member& m, double v0, double v1, int i) {
-  return RMUL(fma(v1, m.deriv_ref[2 * i + 1], RMUL(v0, m.deriv_ref[2 * i])), m.two_over_dx);
-}
-
-struct Q6 {
-  double h0, h1, q0, q1, w0, w1;
-};
-
-#if NH_KP_WARP_XCHG
-// Named-barrier handshakes between neighbouring warps (ids 1..2*(NW-1); 0 is
-// __syncthreads).  A(w): warp w's node-1 side is in smem for warp w+1.
-// B(w): warp w+1's left-face flux is in smem for warp w.
-__device__ __forceinline__ void bar_arrive(int id) {
-  asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory");
-}
-__device__ __forceinline__ void bar_wait(int id) {
-  asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
-}
-#define NH_BAR_A(w) (1 + (w))
-#define NH_BAR_B(w) (NW + (w))
-
-// one Heun stage for the thread's element.  Neighbour exchange inside a warp
-// goes through shuffles; across a warp boundary through two small smem slots
-// per warp and a producer/consumer named barrier with that neighbour only, so
-// warps never wait for the whole CTA.
-template <int KIND>
-__device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q6& q,
-                                           const BottomTime& bt, double x0, double x1,
-                                           const BottomSpace& s0, const BottomSpace& s1, int i,
-                                           int e, int N, double* xs, double* xf, double t6[6],
-                                           double& speed, double& d0, double& d1) {
-  const int lane = i & 31, warp = i >> 5;
-  Bottom6 b0 = bottom_eval_sp_k<KIND>(m, bt, x0, s0);
-  Bottom6 b1 = bottom_eval_sp_k<KIND>(m, bt, x1, s1);
-  Side n0 = make_side(q.h0, q.q0, q.w0, b0.d);
-  Side n1 = make_side(q.h1, q.q1, q.w1, b1.d);
-  // left neighbour's node-1 side (u included: no second division)
-  Side L;
-  L.h = __shfl_up_sync(0xffffffffu, n1.h, 1);
-  L.hu = __shfl_up_sync(0xffffffffu, n1.hu, 1);
-  L.hw = __shfl_up_sync(0xffffffffu, n1.hw, 1);
-  L.d = __shfl_up_sync(0xffffffffu, n1.d, 1);
-  L.u = __shfl_up_sync(0xffffffffu, n1.u, 1);
-  if (lane == 31) {
-    double* x = xs + warp * 5;
-    x[0] = n1.h; x[1] = n1.hu; x[2] = n1.hw; x[3] = n1.d; x[4] = n1.u;
-  }
-  if (warp < NW - 1) bar_arrive(NH_BAR_A(warp));
-  if (warp > 0) {
-    bar_wait(NH_BAR_A(warp - 1));
-    if (lane == 0) {
-      const double* x = xs + (warp - 1) * 5;
-      L.h = x[0]; L.hu = x[1]; L.hw = x[2]; L.d = x[3]; L.u = x[4];
-    }
-  }
-#if NH_STRICT
-  L.rh = 0.0;
-#else
-  L.rh = nh_rcp(L.h);
-#endif
-  if (e == 0) L = ghost_side(n0, m.bc_left);
-  // (CTA slot 0 keeps lane 0's own value: a halo element, never used)
-  double sp;
-  Face fl = face_flux<KIND == NH_BOTTOM_FLAT>(L, n0, g, sp);
-  speed = fmax(speed, sp);
-  Face fr;
-  fr.F1 = __shfl_down_sync(0xffffffffu, fl.F1, 1);
-  fr.F2L = __shfl_down_sync(0xffffffffu, fl.F2L, 1);
-  fr.F3 = __shfl_down_sync(0xffffffffu, fl.F3, 1);
-  fr.F2R = 0.0;
-  if (lane == 0) {
-    double* y = xf + warp * 3;
-    y[0] = fl.F1; y[1] = fl.F2L; y[2] = fl.F3;
-  }
-  if (warp > 0) bar_arrive(NH_BAR_B(warp - 1));
-  if (warp < NW - 1) {
-    bar_wait(NH_BAR_B(warp));
-    if (lane == 31) {
-      const double* y = xf + (warp + 1) * 3;
-      fr.F1 = y[0]; fr.F2L = y[1]; fr.F3 = y[2];
-    }
-  }
-  if (e == N - 1) {
-    fr = face_flux<KIND == NH_BOTTOM_FLAT>(n1, ghost_side(n1, m.bc_right), g, sp);
-    speed = fmax(speed, sp);
-  }
-  element_tendency<KIND == NH_BOTTOM_FLAT>(m, g, n0, n1, fl, fr, b0.d_x, b1.d_x, t6);
-  d0 = b0.d; d1 = b1.d;
-}
-#else
-// one Heun stage for the thread's element: node sides from the registers,
-// left face from the left neighbour's node-1 side (exchanged through smem),
-// right face from the right neighbour's left face (exchanged through smem)
-template <int KIND>
-__device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q6& q,
-                                           const BottomTime& bt, double x0, double x1,
-                                           const BottomSpace& s0, const BottomSpace& s1, int i,
-                                           int e, int N, double* sh, double* sf, double t6[6],
-                                           double& speed, double& d0, double& d1) {
-  Bottom6 b0 = bottom_eval_sp_k<KIND>(m, bt, x0, s0);
-  Bottom6 b1 = bottom_eval_sp_k<KIND>(m, bt, x1, s1);
-  Side n0 = make_side(q.h0, q.q0, q.w0, b0.d);
-  Side n1 = make_side(q.h1, q.q1, q.w1, b1.d);
-  sh[0 * TPB + i] = q.h1; sh[1 * TPB + i] = q.q1; sh[2 * TPB + i] = q.w1; sh[3 * TPB + i] = b1.d;
-  sh[4 * TPB + i] = n1.u;
-  __syncthreads();
-  Side L;
-  if (e == 0) {
-    L = ghost_side(n0, m.bc_left);
-  } else {   // the left neighbour's node-1 side, u included (no second division)
-    int k = i > 0 ? i - 1 : 0;
-    L.h = sh[0 * TPB + k]; L.hu = sh[1 * TPB + k]; L.hw = sh[2 * TPB + k];
-    L.d = sh[3 * TPB + k]; L.u = sh[4 * TPB + k];
-#if NH_STRICT
-    L.rh = 0.0;
-#else
-    L.rh = nh_rcp(L.h);
-#endif
-  }
-  double sp;
-  Face fl = face_flux<KIND == NH_BOTTOM_FLAT>(L, n0, g, sp);
-  speed = fmax(speed, sp);
-  sf[0 * TPB + i] = fl.F1; sf[1 * TPB + i] = fl.F2L; sf[2 * TPB + i] = fl.F3;
-  __syncthreads();
-  Face fr;
-  if (e == N - 1) {
-    fr = face_flux<KIND == NH_BOTTOM_FLAT>(n1, ghost_side(n1, m.bc_right), g, sp);
-    speed = fmax(speed, sp);
-  } else {
-    int k = i < TPB - 1 ? i + 1 : i;
-    fr.F1 = sf[0 * TPB + k]; fr.F2L = sf[1 * TPB + k]; fr.F3 = sf[2 * TPB + k]; fr.F2R = 0.0;
-  }
-  element_tendency<KIND == NH_BOTTOM_FLAT>(m, g, n0, n1, fl, fr, b0.d_x, b1.d_x, t6);
-  d0 = b0.d; d1 = b1.d;
-}
-
-#endif
-
-__device__ __forceinline__ void store_super(double* dst, const Super& s) {
-  dst[0] = s.ga; dst[1] = s.aa; dst[2] = s.ba; dst[3] = s.gz; dst[4] = s.az; dst[5] = s.bz;
-}
-__device__ __forceinline__ Super load_super(const double* s) {
-  return Super{s[0], s[1], s[2], s[3], s[4], s[5]};
-}
-
-// CTA-level reduction of per-element super-elements (1 per thread) into the
-// tile aggregate.  Nodes are stored so that tile_down() can unwind them.
-__device__ __forceinline__ Super tile_up(Super agg, bool tflag, double* wnode, double* wagg,
-                                         double* bnode, int* wflag, int lane, int warp) {
-  const bool wany = __any_sync(0xffffffffu, tflag);
-  double* wn = wnode + warp * 31 * 6;
-  if (wany) {
-    agg = warp_up(agg, wn, lane, 5);
-  } else {
-    unsigned nonid = __ballot_sync(0xffffffffu, !is_identity(agg));
-    int first = nonid ? __ffs(nonid) - 1 : 0;
-    agg = shfl_super(agg, first);
-    if (!nonid) agg = super_identity();
-  }
-  if (lane == 0) {
-    store_super(wagg + warp * 6, agg);
-    wflag[warp] = wany ? 1 : 0;
-  }
-  __syncthreads();
-  Super v = super_identity();
-  if (warp == 0) {
-    if (lane < NW) v = load_super(wagg + lane * 6);
-    v = warp_up(v, bnode, lane, 3);
-  }
-  return v;   // valid in thread 0
-}
-
-}  // namespace
-
-// ---------------------------------------------------------------------- K_P
-struct KpSmem {
-#if NH_KP_WARP_XCHG
-  double sh[2 * TPB];     // (h p) traces of the pending correction
-  double sf[1];
-  double xs[NW * 5];      // per warp: node-1 side of its lane 31
-  double xf[NW * 3];      // per warp: left-face flux of its lane 0
-#else
-  double sh[5 * TPB];
-  double sf[3 * TPB];
-#endif
-  double sk[6 * TPB];     // k1 of this thread's element
-  double sq[6 * TPB];     // step-start state of this thread's element
-  double cfl;             // max wave speed of the tile (CFL = speed dt / dx at the end)
-  uint8_t rf[TPB];
-};
+#include "stream_kp.cuh"
 
 struct KsSmem {
   double wnode[NW * 31 * 6];
@@ -233,234 +31,6 @@ struct KsSmem {
   int wflag[NW];
 };
 
-// Per-thread geometry of a streaming tile.
-struct TileIdx {
-  int b, tile, i, lane, warp, e;
-  bool valid, own;
-  size_t o;
-};
-
-__device__ __forceinline__ TileIdx tile_idx(const StreamArgs& a) {
-  TileIdx t;
-  // grid (tiles, members): no integer division (members past 65535 in z)
-  t.b = blockIdx.z * 65535 + blockIdx.y; t.tile = blockIdx.x;
-  t.i = threadIdx.x; t.lane = t.i & 31; t.warp = t.i >> 5;
-  t.e = t.tile * OWN - H + t.i;
-  t.valid = t.e >= 0 && t.e < a.N;
-  t.own = t.valid && t.i >= H && t.i < H + OWN;
-  t.o = ((size_t)t.b * a.N + (t.valid ? t.e : 0)) * 2;
-  return t;
-}
-
-// Per-member constants of one step, written once per member by K_X (for the
-// next step) or the prep kernel (first step) so tile kernels copy them with
-// the member record instead of recomputing them serially per CTA.
-struct MemberConst {
-  LdgConst lk;        // 8 doubles
-  BottomTime bt0;     // bottom time factors at t
-  BottomTime bt1;     // ... and at t + dt
-  double pad[2];
-};
-static_assert(sizeof(MemberConst) == 16 * 8, "MemberConst is 16 doubles");
-
-__device__ __forceinline__ void member_const(const nh_member& m, const nh_scheme& sch, double t,
-                                             double* out) {
-  MemberConst c;
-  c.lk = make_ldg_const(m.dt, sch.g, sch.rho);
-  c.bt0 = bottom_time(m, t);
-  c.bt1 = bottom_time(m, t + m.dt);
-  c.pad[0] = c.pad[1] = 0.0;
-  *reinterpret_cast<MemberConst*>(out) = c;
-}
-
-// cooperative copy of the member record (39 words) and its step constants (16)
-__device__ __forceinline__ void load_member(const StreamArgs& a, int b, nh_member& msh,
-                                            MemberConst& mc) {
-  constexpr int MW = (int)(sizeof(nh_member) / 8);
-  const int i = threadIdx.x;
-  if (i < MW)
-    reinterpret_cast<unsigned long long*>(&msh)[i] =
-        reinterpret_cast<const unsigned long long*>(a.members + b)[i];
-  else if (i < MW + 16)
-    reinterpret_cast<unsigned long long*>(&mc)[i - MW] =
-        reinterpret_cast<const unsigned long long*>(a.mconst + (size_t)b * 16)[i - MW];
-}
-
-template <int KIND>
-__device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
-                                        const MemberConst& mc, const TileIdx& ti, Q6 q,
-                                        KpSmem& ks) {
-  double* sh = ks.sh;
-  double* sf = ks.sf;
-  uint8_t* rf = ks.rf;
-#if NH_KP_WARP_XCHG
-  double* XS = ks.xs;
-  double* XF = ks.xf;
-  (void)sf;
-#else
-  double* XS = sh;
-  double* XF = sf;
-#endif
-  double& cfl_sh = ks.cfl;
-
-  const int N = a.N, T = a.tiles;
-  const int b = ti.b, tile = ti.tile, i = ti.i, lane = ti.lane, e = ti.e;
-  const bool valid = ti.valid, own = ti.own;
-  const size_t o = ti.o;
-  const nh_scheme& sch = a.sch;
-  const double g = sch.g;
-  nh_status* st = a.status + b;
-  const int step = a.step_counter ? a.step_counter[b] : 0;
-
-  const double dt = m.dt;
-  const double ed = (double)e;
-  const double x0 = sample_xd(m, ed, 0), x1 = sample_xd(m, ed, 1);
-  const BottomSpace s0 = bottom_space_k<KIND>(m, x0), s1 = bottom_space_k<KIND>(m, x1);
-  double speed = 0.0;
-
-  // ---------------- Heun stage 1 at t ----------------
-  // positivity (hydrostatic.py:101-103, 216-217) gathered into one report
-  unsigned bad = (own && (q.h0 <= 0.0 || q.h1 <= 0.0)) ? 1u : 0u;
-  ks.sq[0 * TPB + i] = q.h0; ks.sq[1 * TPB + i] = q.h1; ks.sq[2 * TPB + i] = q.q0;
-  ks.sq[3 * TPB + i] = q.q1; ks.sq[4 * TPB + i] = q.w0; ks.sq[5 * TPB + i] = q.w1;
-  Q6 qs;
-  {
-    double k1[6], dd0, dd1;
-    stage_tend<KIND>(m, g, q, mc.bt0, x0, x1, s0, s1, i, e, N, XS, XF, k1, speed, dd0, dd1);
-#pragma unroll
-    for (int f = 0; f < 6; ++f) ks.sk[f * TPB + i] = k1[f];
-    qs = Q6{RADD(q.h0, RMUL(dt, k1[0])), RADD(q.h1, RMUL(dt, k1[1])),
-            RADD(q.q0, RMUL(dt, k1[2])), RADD(q.q1, RMUL(dt, k1[3])),
-            RADD(q.w0, RMUL(dt, k1[4])), RADD(q.w1, RMUL(dt, k1[5]))};
-  }
-  bad |= (own && !(qs.h0 > 0.0 && qs.h1 > 0.0)) ? 2u : 0u;
-#if !NH_KP_WARP_XCHG
-  __syncthreads();   // every read of sh / sf of stage 1 is done
-#endif
-
-  // ---------------- Heun stage 2 at t + dt ----------------
-  double k2[6], d0, d1;   // d0, d1: depth at t + dt, reused by the criterion
-  {
-    double dummy = 0.0;
-    stage_tend<KIND>(m, g, qs, mc.bt1, x0, x1, s0, s1, i, e, N, XS, XF, k2, dummy, d0, d1);
-  }
-  double qv[6];
-#pragma unroll
-  for (int f = 0; f < 6; ++f)
-    qv[f] = RADD(ks.sq[f * TPB + i], RMUL(dt, RMUL(0.5, RADD(ks.sk[f * TPB + i], k2[f]))));
-  Q6 qp{qv[0], qv[1], qv[2], qv[3], qv[4], qv[5]};
-  bad |= (own && !(qp.h0 > 0.0 && qp.h1 > 0.0)) ? 4u : 0u;
-  if (bad)   // the reference raises at the first failing check: lowest code wins
-    nh_report(st, step,
-              (bad & 1u) ? NH_ERR_POSITIVITY_ENTRY
-                         : ((bad & 2u) ? NH_ERR_POSITIVITY_STAGE1 : NH_ERR_POSITIVITY_STAGE2),
-              (bad & 1u) ? e : -1);
-  if (own) {
-    *reinterpret_cast<double2*>(a.h_out + o) = double2{qp.h0, qp.h1};
-    *reinterpret_cast<double2*>(a.hu_out + o) = double2{qp.q0, qp.q1};
-    *reinterpret_cast<double2*>(a.hw_out + o) = double2{qp.w0, qp.w1};
-  }
-  if (sch.record_cfl) {
-    // max wave speed over the warp on the bit patterns (speeds are >= 0, so
-    // the unsigned order is the numeric order): high words, then low words of
-    // the lanes holding the maximal high word.  Halo lanes contribute 0.
-    const unsigned long long u = (unsigned long long)__double_as_longlong(own ? speed : 0.0);
-    const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(u >> 32));
-    const unsigned lo = __reduce_max_sync(0xffffffffu, (unsigned)(u >> 32) == hi ? (unsigned)u : 0u);
-    if (lane == 0 && (hi | lo))
-      atomicMax((unsigned long long*)&cfl_sh, ((unsigned long long)hi << 32) | lo);
-  }
-  // CFL of the tile = (max speed) dt / dx: rounding is monotone, so this is
-  // the max over elements of the per-element speed dt / dx (hydrostatic.py CFL check)
-  auto publish_cfl = [&]() {
-    if (i == 0 && cfl_sh > 0.0) {
-      const double c = cfl_sh * dt / m.dx;
-      atomicMax((unsigned long long*)&st->cfl_max, (unsigned long long)__double_as_longlong(c));
-    }
-  };
-  if (sch.mode == NH_MODE_HYDROSTATIC) {
-    __syncthreads();
-    publish_cfl();
-    return;
-  }
-
-  // ---------------- criterion on the predictor (t + dt) ----------------
-  uint8_t raw = 0;
-  if (valid) {
-    if (sch.mode == NH_MODE_GLOBAL) {
-      raw = 1;
-    } else {
-      double v0, v1;
-      switch (sch.criterion) {
-        case NH_CRIT_ETA_OVER_D: {
-          v0 = fabs(RDIVP(RSUB(qp.h0, d0), d0)); v1 = fabs(RDIVP(RSUB(qp.h1, d1), d1));
-          break;
-        }
-        case NH_CRIT_ETA_X: {
-          v0 = fabs(ederiv(m, RSUB(qp.h0, d0), RSUB(qp.h1, d1), 0));
-          v1 = fabs(ederiv(m, RSUB(qp.h0, d0), RSUB(qp.h1, d1), 1));
-          break;
-        }
-        case NH_CRIT_U:
-          v0 = fabs(RDIVP(qp.q0, qp.h0)); v1 = fabs(RDIVP(qp.q1, qp.h1));
-          break;
-        case NH_CRIT_U_X: {
-          double u0 = RDIVP(qp.q0, qp.h0), u1 = RDIVP(qp.q1, qp.h1);
-          v0 = fabs(ederiv(m, u0, u1, 0)); v1 = fabs(ederiv(m, u0, u1, 1));
-          break;
-        }
-        case NH_CRIT_W:
-          v0 = fabs(RDIVP(qp.w0, qp.h0)); v1 = fabs(RDIVP(qp.w1, qp.h1));
-          break;
-        default: {
-          double w0 = RDIVP(qp.w0, qp.h0), w1 = RDIVP(qp.w1, qp.h1);
-          v0 = fabs(ederiv(m, w0, w1, 0)); v1 = fabs(ederiv(m, w0, w1, 1));
-          break;
-        }
-      }
-      raw = fmax(v0, v1) > sch.k_nh ? 1 : 0;
-    }
-  }
-  rf[i] = raw;
-  __syncthreads();
-  const bool enl = sch.mode == NH_MODE_ADAPTIVE && sch.enlarge;
-  auto eff = [&](int s) -> bool {
-    int ee = tile * OWN - H + s;
-    if (ee < 0 || ee >= N || s < 0 || s >= TPB) return false;
-    bool f = rf[s] != 0;
-    if (enl) {
-      if (ee > 0 && s > 0) f = f || rf[s - 1];
-      if (ee < N - 1 && s + 1 < TPB) f = f || rf[s + 1];
-    }
-    return f;
-  };
-  const bool flag = own && eff(i);
-  if (own) a.flags_cur[(size_t)b * N + e] = flag ? 1 : 0;
-  if (flag && a.flag_bits) {
-    uint32_t* fb = a.flag_bits + ((size_t)step * a.B + b) * ((N + 31) / 32);
-    atomicOr(fb + (e >> 5), 1u << (e & 31));
-  }
-
-  // ---------------- per-tile flagged count; unflagged tiles aggregate to a gap ----------------
-  {
-    int nf = __syncthreads_count(flag);
-    if (i == H) {   // first own slot
-      double* ta = a.tile_agg + ((size_t)b * T + tile) * 8;
-      ta[6] = (double)nf;
-      if (nf == 0) store_super(ta, super_gap(qp.q0));
-      if (nf) {
-        atomicAdd((unsigned long long*)&st->flagged, (unsigned long long)nf);
-        a.tile_list[atomicAdd(a.tile_count, 1)] = b * T + tile;   // work list of K_S / K_C
-      }
-    }
-    // right-end ghost outer trace (corrector.py:400-402)
-    if (e == N - 1 && own) {
-      double qq = qp.q1;
-      a.tile_agg[((size_t)b * T + tile) * 8 + 7] = (m.bc_right == NH_BC_WALL) ? -qq : qq;
-    }
-  }
-  publish_cfl();
-}
 
 // ---------------------------------------------------------------------- K_S
 // Tiles holding flagged elements: LDG coefficients at t+dt and the per-element
@@ -538,94 +108,6 @@ __global__ void __launch_bounds__(TPB, NH_KS_MIN_BLOCKS) nh_stream_ks(StreamArgs
   }
 }
 
-__global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(StreamArgs a) {
-  __shared__ nh_member msh;
-  __shared__ MemberConst mc;
-  __shared__ KpSmem ks;
-  const TileIdx ti = tile_idx(a);
-  if (ti.b >= a.B) return;   // padding of the (tiles, 65535, z) grid
-  const int N = a.N, i = ti.i, b = ti.b, e = ti.e;
-
-  // state and the previous step's pending record are requested first so their
-  // latency overlaps the member-record copy and the per-CTA constants
-  Q6 q{1.0, 1.0, 0.0, 0.0, 0.0, 0.0};
-  if (ti.valid) {
-    double2 vh = *reinterpret_cast<const double2*>(a.h_in + ti.o);
-    double2 vq = *reinterpret_cast<const double2*>(a.hu_in + ti.o);
-    double2 vw = *reinterpret_cast<const double2*>(a.hw_in + ti.o);
-    q = Q6{vh.x, vh.y, vq.x, vq.y, vw.x, vw.y};
-  }
-  const bool f = a.pend && ti.valid && a.flags_prev[(size_t)b * N + e];
-  double p0 = 0.0, p1 = 0.0, phi0 = 0.0, phi1 = 0.0, dx0 = 0.0, dx1 = 0.0;
-  if (f) {
-    const size_t BN = (size_t)a.B * N;
-    const double* pv = a.pend + (size_t)b * N + e;
-    p0 = pv[0]; p1 = pv[BN]; phi0 = pv[2 * BN]; phi1 = pv[3 * BN]; dx0 = pv[4 * BN]; dx1 = pv[5 * BN];
-  }
-  load_member(a, b, msh, mc);
-  const double hp0 = q.h0 * p0, hp1 = q.h1 * p1;
-  if (a.pend) {
-    ks.sh[0 * TPB + i] = hp0;
-    ks.sh[1 * TPB + i] = hp1;
-  }
-  if (i == 0) ks.cfl = 0.0;
-  __syncthreads();
-
-  // ---------------- pending correction of the previous step ----------------
-  // hw += dt/rho (6/quad p + d_x/quad (h p)_x + phi) on flagged elements
-  // (corrector.py:441-482); (h p)_x lifts use the neighbours' (h p) traces.
-  double bp0 = 0.0, bp1 = 0.0;
-  if (f) {
-    const double* sh = ks.sh;
-    auto hp_of = [&](int ee, int node, int slot) -> double {
-      if (slot >= 0 && slot < TPB) return sh[node * TPB + slot];
-      // neighbour outside the CTA's slots (never needed for own elements)
-      if (!a.flags_prev[(size_t)b * N + ee]) return 0.0;
-      size_t oo = ((size_t)b * N + ee) * 2 + node;
-      return a.h_in[oo] * a.pend[(size_t)node * a.B * N + (size_t)b * N + ee];
-    };
-    double hx0 = ederiv(msh, hp0, hp1, 0), hx1 = ederiv(msh, hp0, hp1, 1);
-    if (e < N - 1) {
-      double hr = hp_of(e + 1, 0, i + 1);
-      double avg = 0.5 * (hp1 + hr);
-      hx0 += (avg - hp1) * msh.lift_right[0];
-      hx1 += (avg - hp1) * msh.lift_right[1];
-    }
-    if (e > 0) {
-      double hl = hp_of(e - 1, 1, i - 1);
-      double avg = 0.5 * (hl + hp0);
-      hx0 -= (avg - hp0) * msh.lift_left[0];
-      hx1 -= (avg - hp0) * msh.lift_left[1];
-    }
-    double qd0 = 4.0 + dx0 * dx0, qd1 = 4.0 + dx1 * dx1;
-    bp0 = nh_div(6.0, qd0) * p0 + nh_div(dx0, qd0) * hx0 + phi0;
-    bp1 = nh_div(6.0, qd1) * p1 + nh_div(dx1, qd1) * hx1 + phi1;
-  }
-  __syncthreads();   // every read of the (h p) traces done before sh is reused
-  if (f) {
-    q.w0 += mc.lk.cdt * bp0;
-    q.w1 += mc.lk.cdt * bp1;
-  }
-  if (a.finalize) {
-    if (ti.own) {
-      double2 vw{q.w0, q.w1};
-      *reinterpret_cast<double2*>(const_cast<double*>(a.hw_in) + ti.o) = vw;
-    }
-    return;
-  }
-#if NH_KP_RUNTIME_KIND
-  kp_body<-1>(a, msh, mc, ti, q, ks);
-#else
-  switch (msh.bottom_kind) {
-    case NH_BOTTOM_FLAT: kp_body<NH_BOTTOM_FLAT>(a, msh, mc, ti, q, ks); break;
-    case NH_BOTTOM_PLATE: kp_body<NH_BOTTOM_PLATE>(a, msh, mc, ti, q, ks); break;
-    case NH_BOTTOM_QUARTIC_SLIDE: kp_body<NH_BOTTOM_QUARTIC_SLIDE>(a, msh, mc, ti, q, ks); break;
-    case NH_BOTTOM_SMOOTH_BOX: kp_body<NH_BOTTOM_SMOOTH_BOX>(a, msh, mc, ti, q, ks); break;
-    default: kp_body<NH_BOTTOM_SLOPE_SLIDE>(a, msh, mc, ti, q, ks); break;
-  }
-#endif
-}
-
 // ---------------------------------------------------------------------- K_X
 // One warp per member: chain of its T tile aggregates (lane l folds tiles
 // [l*cpl, (l+1)*cpl)), merge tree across lanes, back-substitution, then each
@@ -676,6 +158,32 @@ __global__ void __launch_bounds__(256) nh_stream_kx(StreamArgs a) {
 __global__ void __launch_bounds__(256) nh_stream_prep(StreamArgs a) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < a.B) member_const(a.members[b], a.sch, a.time[b], a.mconst + (size_t)b * 16);
+}
+
+// Members grouped by bottom kind (stable within a kind), one 1024-thread CTA.
+__global__ void __launch_bounds__(1024) nh_stream_order(StreamArgs a) {
+  __shared__ int wsum[32];
+  __shared__ int base;
+  const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  if (i == 0) base = 0;
+  __syncthreads();
+  for (int kind = 0; kind <= NH_BOTTOM_SLOPE_SLIDE + 1; ++kind) {
+    for (int c = 0; c < a.B; c += 1024) {
+      const int b = c + i;
+      int k = b < a.B ? a.members[b].bottom_kind : -1;
+      if (k < 0 || k > NH_BOTTOM_SLOPE_SLIDE) k = NH_BOTTOM_SLOPE_SLIDE + 1;
+      const bool mine = b < a.B && k == kind;
+      const unsigned bal = __ballot_sync(0xffffffffu, mine);
+      if (lane == 0) wsum[warp] = __popc(bal);
+      __syncthreads();
+      int pre = 0, tot = 0;
+      for (int w = 0; w < 32; ++w) { pre += w < warp ? wsum[w] : 0; tot += wsum[w]; }
+      if (mine) const_cast<int*>(a.order)[base + pre + __popc(bal & ((1u << lane) - 1u))] = b;
+      __syncthreads();
+      if (i == 0) base += tot;
+      __syncthreads();
+    }
+  }
 }
 
 // ---------------------------------------------------------------------- K_C
@@ -776,10 +284,11 @@ int nh_launch_gather_p(const double* pend, const uint8_t* flags, double* p, size
 
 void* nh_stream_kernel(int which) {
   switch (which) {
-    case 0: return (void*)nh_stream_kp;
+    case 0: return nh_stream_kp_ptr();
     case 1: return (void*)nh_stream_kx;
     case 3: return (void*)nh_stream_ks;
     case 4: return (void*)nh_stream_prep;
+    case 5: return (void*)nh_stream_order;
     default: return (void*)nh_stream_kc;
   }
 }

@@ -46,11 +46,14 @@ struct StreamArgs {
   int* tile_list;              // [B*T] tiles holding a flagged element (this step, any order)
   int* tile_count;             // entries of tile_list (K_P appends, K_S / K_C consume)
   int* tile_count_next;        // the next step's counter, zeroed by K_X
+  const int* order;            // [B] K_P's member order (grouped by bottom kind), or NULL
   nh_scheme sch;
   int B, N, tiles, finalize;
 };
 
-// which: 0 K_P, 1 K_X, 2 K_C, 3 K_S, 4 prep (step constants for the current time)
+// which: 0 K_P, 1 K_X, 2 K_C, 3 K_S, 4 prep (step constants for the current time),
+//        5 order (members grouped by bottom kind, one CTA)
 void* nh_stream_kernel(int which);
+void* nh_stream_kp_ptr();   // stream_kp.cu
 int nh_launch_gather_p(const double* pend, const uint8_t* flags, double* p, size_t n,
                        cudaStream_t s);

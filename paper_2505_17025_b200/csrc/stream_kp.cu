@@ -1,0 +1,17 @@
+// K_P of the streaming step (body in stream_kp.cuh); its own translation unit.
+#include "stream_kp.cuh"
+
+__global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(StreamArgs a) {
+  __shared__ nh_member msh;
+  __shared__ MemberConst mc;
+  __shared__ KpSmem ks;
+  // grid (tiles, members): no integer division (members past 65535 in z);
+  // the member axis runs in bottom-kind order so the CTAs resident at one
+  // time mostly execute the same kind-specialised body (instruction cache)
+  int b = blockIdx.z * 65535 + blockIdx.y;
+  if (b >= a.B) return;   // padding of the (tiles, 65535, z) grid
+  if (a.order) b = a.order[b];
+  kp_tile(a, tile_idx(a, b, blockIdx.x), msh, mc, ks);
+}
+
+void* nh_stream_kp_ptr() { return (void*)nh_stream_kp; }
