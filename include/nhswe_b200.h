@@ -147,6 +147,14 @@ int nh_stream_advance(const nh_member* members, int n_members, int n_elements,
                       void* stream);
 size_t nh_stream_workspace_bytes(int n_members, int n_elements);
 
+/* Time loop of nh_stream_advance as a CUDA graph (default on; the
+ * NH_STREAM_GRAPH=0 environment variable turns it off at load).  With
+ * graphs on and per-kernel timing off, runs of >= 5 steps launch step 0,
+ * then replay one captured graph of an (odd, even) step pair -- the ping-pong
+ * buffers repeat with period 2 -- and launch a trailing odd step directly.
+ * enable: 1 on, 0 off, -1 query.  Returns the previous setting. */
+int nh_stream_graphs(int enable);
+
 /* Per-kernel CUDA-event timing of nh_stream_advance (diagnostics for the
  * roofline report).  nh_stream_timing(1) clears and arms the recorder; every
  * later nh_stream_advance brackets each launch with events on its stream.

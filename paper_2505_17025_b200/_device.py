@@ -206,6 +206,11 @@ STREAM_KERNELS = ("nh_stream_kp", "nh_stream_ks", "nh_stream_kx", "nh_stream_kc"
                   "nh_stream_kp_finalize", "nh_stream_prep")
 
 
+def stream_graphs(enable: bool | None = None) -> bool:
+    """Query / set whether nh_stream_advance runs its time loop as a CUDA graph."""
+    return bool(require_cuda().nh_stream_graphs(-1 if enable is None else int(bool(enable))))
+
+
 def stream_timing(enable: bool):
     """Arm / disarm per-kernel CUDA-event timing inside nh_stream_advance."""
     _lib.check(require_cuda().nh_stream_timing(1 if enable else 0), "nh_stream_timing")

@@ -53,7 +53,8 @@ class Outputs(ctypes.Structure):
 EXPORTS = ("nh_abi_version", "nh_advance", "nh_stream_advance", "nh_stream_workspace_bytes",
            "nh_rhs", "nh_criterion", "nh_coefficients",
            "nh_ldg_solve", "nh_correct_momentum", "nh_bottom_sample", "nh_plan",
-           "nh_last_cuda_error", "nh_stream_timing", "nh_stream_kernel_times", "nh_launch_count",
+           "nh_last_cuda_error", "nh_stream_graphs", "nh_stream_timing", "nh_stream_kernel_times",
+           "nh_launch_count",
            "nh_selftest_arith")
 
 _P = ctypes.c_void_p
@@ -66,6 +67,7 @@ _SIGS = {
     "nh_stream_advance": ([_P, _I, _I, _P, _P, _P, _P, _I, ctypes.POINTER(Scheme),
                            ctypes.POINTER(Outputs), _P, _P, ctypes.c_size_t, _P], _I),
     "nh_stream_workspace_bytes": ([_I, _I], ctypes.c_size_t),
+    "nh_stream_graphs": ([_I], _I),
     "nh_stream_timing": ([_I], _I),
     "nh_stream_kernel_times": ([_P, _P], _I),
     "nh_launch_count": ([], ctypes.c_longlong),

@@ -6,6 +6,7 @@
 #include <mutex>
 #include <vector>
 #include <cstdlib>
+#include <cstring>
 #include "step_kernel.cuh"
 #include "stream_kernels.cuh"
 
@@ -270,6 +271,69 @@ int nh_bottom_sample(const nh_member* members, int n_members, const double* x, i
   return counted(nh_launch_bottom(members, n_members, x, n_points, time, out, (cudaStream_t)stream));
 }
 
+// ------------------------------------------------------------- CUDA graphs
+extern "C++" {
+namespace {
+// NH_STREAM_GRAPH=0 disables the captured time loop (plain launches).
+std::atomic<int> g_graphs{-1};
+bool graphs_enabled() {
+  if (g_graphs.load() < 0)
+    g_graphs = (!getenv("NH_STREAM_GRAPH") || atoi(getenv("NH_STREAM_GRAPH")) != 0) ? 1 : 0;
+  return g_graphs.load() != 0;
+}
+
+// One cached executable graph of a pair of steps, keyed on the launch
+// arguments of both steps (a new ensemble, buffer or scheme re-captures).
+struct PairGraph {
+  bool valid = false;
+  unsigned char key[sizeof(StreamArgs)];
+  cudaGraphExec_t exec = nullptr;
+  long long nodes = 0;
+  cudaStream_t cap = nullptr;
+} g_pair;
+std::mutex g_pair_mu;
+
+template <class Capture>
+int pair_graph(const StreamArgs& a, Capture capture, cudaGraphExec_t& exec, long long& nodes) {
+  std::lock_guard<std::mutex> lk(g_pair_mu);
+  if (!g_pair.cap && cudaStreamCreateWithFlags(&g_pair.cap, cudaStreamNonBlocking) != cudaSuccess)
+    return NH_E_CUDA;
+  // capture (nothing executes) on a private stream: the caller's may be the
+  // legacy default stream, which cannot be captured; the graph is launched
+  // on the caller's stream
+  const long long l0 = g_launches.load();
+  if (cudaStreamBeginCapture(g_pair.cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return NH_E_CUDA;
+  int rc = capture(g_pair.cap);
+  cudaGraph_t graph = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(g_pair.cap, &graph);
+  const long long n = g_launches.load() - l0;
+  g_launches -= n;   // captured, not executed
+  if (rc || ce != cudaSuccess || !graph) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc ? rc : NH_E_CUDA;
+  }
+  // `a` now holds the even step's arguments, which fix the odd step's too
+  if (g_pair.valid && std::memcmp(&a, g_pair.key, sizeof(StreamArgs)) == 0) {
+    cudaGraphDestroy(graph);
+  } else {
+    if (g_pair.exec) cudaGraphExecDestroy(g_pair.exec);
+    g_pair.exec = nullptr;
+    g_pair.valid = false;
+    ce = cudaGraphInstantiate(&g_pair.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) return NH_E_CUDA;
+    std::memcpy(g_pair.key, &a, sizeof(StreamArgs));
+    g_pair.valid = true;
+    g_pair.nodes = n;
+  }
+  exec = g_pair.exec;
+  nodes = g_pair.nodes;
+  return 0;
+}
+}  // namespace
+}  // extern "C++"
+
 // ------------------------------------------------------------- streaming path
 static int stream_tiles(int n) { return (n + NH_STREAM_OWN - 1) / NH_STREAM_OWN; }
 
@@ -326,7 +390,8 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   }
   double* A[3] = {h, hu, hw};
   double* Bb[3] = {alt, alt + 2 * BN, alt + 4 * BN};
-  StreamArgs a = {};
+  StreamArgs a;
+  std::memset(&a, 0, sizeof a);   // padding too: the graph cache compares bytes
   a.members = members; a.time = time; a.status = status; a.step_counter = counter;
   a.scratch = scratch; a.tile_agg = tagg; a.tile_io = tio;
   a.flag_bits = outputs ? outputs->flag_bits : nullptr;
@@ -349,10 +414,12 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
     if (a.order)
       if (int rc = stream_launch(nh_stream_kernel(5), 5, dim3(1), dim3(1024), args, s)) return rc;
   }
-  int cur = 0;   // 0: state in A, 1: state in Bb
-  for (int k = 0; k < n_steps; ++k) {
-    double** in = cur ? Bb : A;
-    double** out = cur ? A : Bb;
+  // step k reads the state written by step k - 1: ping-pong A <-> Bb, and
+  // the pending record / flags / flagged-tile counters alternate the same way,
+  // so every step's launches depend only on k's parity (k > 0)
+  auto set_step = [&](int k) {
+    double** in = (k & 1) ? Bb : A;
+    double** out = (k & 1) ? A : Bb;
     a.h_in = in[0]; a.hu_in = in[1]; a.hw_in = in[2];
     a.h_out = out[0]; a.hu_out = out[1]; a.hw_out = out[2];
     a.pend = (corr && k > 0) ? pend[(k - 1) & 1] : nullptr;
@@ -361,14 +428,39 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
     a.flags_cur = flags[k & 1];
     a.tile_count = tcount + (k & 1);
     a.tile_count_next = tcount + ((k + 1) & 1);
+  };
+  auto launch_step = [&](int k, cudaStream_t st) -> int {
+    set_step(k);
     void* args[1] = {&a};
-    int rc = stream_launch(kp, 0, gp, bp, args, s);
-    if (!rc && corr) rc = stream_launch(ks, 1, gs, bp, args, s);
-    if (!rc) rc = stream_launch(kx, 2, gx, bx, args, s);
-    if (!rc && corr) rc = stream_launch(kc, 3, gc, bp, args, s);
-    if (rc) return rc;
-    cur ^= 1;
+    int rc = stream_launch(kp, 0, gp, bp, args, st);
+    if (!rc && corr) rc = stream_launch(ks, 1, gs, bp, args, st);
+    if (!rc) rc = stream_launch(kx, 2, gx, bx, args, st);
+    if (!rc && corr) rc = stream_launch(kc, 3, gc, bp, args, st);
+    return rc;
+  };
+  if (graphs_enabled() && !g_timing.on && n_steps >= 5) {
+    // the time loop as a CUDA graph: step 0 directly, then one captured
+    // (odd, even) pair of steps replayed, then a trailing odd step if any
+    if (int rc = launch_step(0, s)) return rc;
+    cudaGraphExec_t exec = nullptr;
+    long long nodes = 0;
+    if (int rc = pair_graph(a, [&](cudaStream_t cs) -> int {
+          int r = launch_step(1, cs);
+          return r ? r : launch_step(2, cs);
+        }, exec, nodes))
+      return rc;
+    const int pairs = (n_steps - 1) / 2;
+    for (int r = 0; r < pairs; ++r) {
+      if (cudaGraphLaunch(exec, s) != cudaSuccess) return NH_E_CUDA;
+      g_launches += nodes;
+    }
+    if ((n_steps - 1) & 1)
+      if (int rc = launch_step(n_steps - 1, s)) return rc;
+  } else {
+    for (int k = 0; k < n_steps; ++k)
+      if (int rc = launch_step(k, s)) return rc;
   }
+  const int cur = n_steps & 1;   // 1: the final state is in Bb
   double** fin = cur ? Bb : A;
   if (corr) {   // apply the last pending vertical-momentum update in place
     a.h_in = fin[0]; a.hu_in = fin[1]; a.hw_in = fin[2];
@@ -390,6 +482,12 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
     ++g_launches;
   }
   return 0;
+}
+
+int nh_stream_graphs(int enable) {
+  const int prev = graphs_enabled() ? 1 : 0;
+  if (enable >= 0) g_graphs = enable ? 1 : 0;
+  return prev;
 }
 
 int nh_stream_timing(int enable) {

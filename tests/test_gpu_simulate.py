@@ -174,3 +174,34 @@ def test_stream_member_chunks_bitwise_equal():
     for other in out[1:]:
         for a, b in zip(out[0], other):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("n_steps", [5, 6, 61])
+@pytest.mark.parametrize("mode", ["adaptive", "global", "hydrostatic"])
+def test_stream_graph_bitwise_equal_to_launches(n_steps, mode):
+    """The time loop captured as a CUDA graph of step pairs (nh_stream_graphs)
+    gives bit-identical states, times, flag counts and launch counts to plain
+    launches, for even and odd step counts and repeated calls (cached graph)."""
+    from paper_2505_17025_b200 import _device as D
+    cfg = configs.Config4(n_members=6, n_elements=700, n_steps=n_steps)
+    recs = cfg.records()
+    states = [cfg.host_state(i, oracle_depth) for i in range(cfg.n_members)]
+    H, Q, W = (np.stack([s[k] for s in states]) for k in range(3))
+    crit = P.Criterion("eta_over_d") if mode == "adaptive" else None
+    prev = D.stream_graphs()
+    out = []
+    try:
+        for graphs in (False, True):
+            D.stream_graphs(graphs)
+            ens = P.Ensemble.from_host(recs, H, Q, W)
+            l0 = D.launch_count()
+            for _ in range(2):
+                ens.advance(n_steps, mode, crit, path="stream")
+            launches = D.launch_count() - l0
+            st = ens.check()
+            out.append((ens.h.cpu().numpy(), ens.hu.cpu().numpy(), ens.hw.cpu().numpy(),
+                        ens.time.cpu().numpy(), st["flagged"].copy(), launches))
+    finally:
+        D.stream_graphs(prev)
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(a, b)

@@ -1,0 +1,48 @@
+"""Config 3 chaos check (CPU, oracle = the reference's arithmetic bit for bit):
+restart the oracle from the reference's step-S checkpoint with one h value
+perturbed by 1 ulp and run to the final step, recording the per-step flagged
+count.  Prints the full-run mask fraction mean of the perturbed trajectory
+(reference counts for steps <= S) next to the reference's own.
+
+    python tools/config3_perturbed.py [S] [element]  > profiles/r1_config3_perturbed.txt
+"""
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle import nhswe_oracle as O  # noqa: E402
+from paper_2505_17025_b200 import configs  # noqa: E402
+from tests.helpers import oracle_member  # noqa: E402
+
+S = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
+E = int(sys.argv[2]) if len(sys.argv) > 2 else 1500
+G = np.load(os.path.join(os.path.dirname(__file__), "..", "tests", "golden", "config3_full.npz"))
+cfg = configs.config3()
+m = cfg.member(0)
+mem = oracle_member(m.grid, m.bathymetry, m.bcs, m.dt)
+r = G[f"ck/s{S}"]
+t = float(G[f"ck/t{S}"])
+h, hu, hw = r[0].copy(), r[1].copy(), r[2].copy()
+h[E, 0] = np.nextafter(h[E, 0], np.inf)
+n = int(G["n_steps"])
+ref_counts = G["adaptive/flag_count"].astype(np.int64)
+counts = list(ref_counts[:S])
+t0 = time.time()
+for k in range(S, n):
+    o = O.step(mem, h, hu, hw, t, "adaptive", cfl_warn=False)
+    h, hu, hw = o.h, o.hu, o.hw
+    t = t + mem.dt
+    counts.append(int(o.flags.sum()))
+    if (k + 1) % 10000 == 0:
+        c = np.array(counts)
+        print(f"step {k + 1}: running mask fraction perturbed {c.mean() / m.grid.n_elements:.4f} "
+              f"reference {ref_counts[:k + 1].mean() / m.grid.n_elements:.4f} "
+              f"({time.time() - t0:.0f}s)", flush=True)
+c = np.array(counts)
+print(f"final: mask fraction mean perturbed {c.mean() / m.grid.n_elements:.4f}, reference "
+      f"{float(G['adaptive/mask_fraction']):.4f}; final eta max |.| perturbed "
+      f"{np.abs(h - O.depth_of(mem, t) if hasattr(O, 'depth_of') else h).max():.4f}")
+np.save("/tmp/config3_perturbed_counts.npy", c)
