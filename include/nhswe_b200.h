@@ -135,7 +135,7 @@ int nh_advance(const nh_member* members, int n_members, int n_elements,
 /* Streaming variant of nh_advance for large ensembles (same contract and
  * in-place semantics; modes HYDROSTATIC / GLOBAL / ADAPTIVE with the
  * eta_over_d, eta_x, u, u_x criteria).  Every step is four kernels over
- * independent 248-element tiles (K_P predictor+criterion, K_S condensation,
+ * independent 120-element tiles of 128 threads (K_P predictor+criterion, K_S condensation,
  * K_X per-member tile chain, K_C reconstruction) with the vertical-momentum
  * update fused into the next step's load; state goes through HBM once per
  * step.  `workspace` is device memory of at least

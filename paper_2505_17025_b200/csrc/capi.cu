@@ -110,7 +110,7 @@ int counted(int rc) {
 }
 
 // enqueue a plain launch of a streaming kernel, bracketing it with events when timing
-int stream_launch(void* k, int kid, dim3 g, dim3 b, void** args, cudaStream_t s) {
+int stream_launch(void* k, int kid, dim3 g, dim3 b, void** args, cudaStream_t s, size_t smem = 0) {
   size_t a = 0;
   if (g_timing.on) {
     if (g_timing.used == 0 || g_timing.marks.empty() || g_timing.marks.back().b != g_timing.used - 1) {
@@ -119,7 +119,7 @@ int stream_launch(void* k, int kid, dim3 g, dim3 b, void** args, cudaStream_t s)
     }
     a = g_timing.used - 1;
   }
-  if (cudaLaunchKernel(k, g, b, args, 0, s) != cudaSuccess) return NH_E_CUDA;
+  if (cudaLaunchKernel(k, g, b, args, smem, s) != cudaSuccess) return NH_E_CUDA;
   ++g_launches;
   if (g_timing.on) {
     cudaEvent_t e = g_timing.next();
@@ -381,6 +381,9 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nks, nh_stream_kernel(3), NH_STREAM_THREADS, 0) != cudaSuccess ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nkc, nh_stream_kernel(2), NH_STREAM_THREADS, 0) != cudaSuccess)
       return NH_E_CUDA;
+    if (cudaFuncSetAttribute(nh_stream_kernel(0), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)nh_stream_kp_smem()) != cudaSuccess)
+      return NH_E_CUDA;
     ks_grid = std::max(1, nks) * sms;
     kc_grid = std::max(1, nkc) * sms;
     if (const char* v = getenv("NH_KS_WAVES")) {   // diagnostics: grid = waves x resident CTAs
@@ -403,6 +406,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
       gx((B + 7) / 8), bx(256);
   const dim3 gs((unsigned)std::min<size_t>(ks_grid, BT)), gc((unsigned)std::min<size_t>(kc_grid, BT));
   void* kp = nh_stream_kernel(0);
+  const size_t kp_smem = nh_stream_kp_smem();
   void* kx = nh_stream_kernel(1);
   void* kc = nh_stream_kernel(2);
   void* ks = nh_stream_kernel(3);
@@ -432,7 +436,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   auto launch_step = [&](int k, cudaStream_t st) -> int {
     set_step(k);
     void* args[1] = {&a};
-    int rc = stream_launch(kp, 0, gp, bp, args, st);
+    int rc = stream_launch(kp, 0, gp, bp, args, st, kp_smem);
     if (!rc && corr) rc = stream_launch(ks, 1, gs, bp, args, st);
     if (!rc) rc = stream_launch(kx, 2, gx, bx, args, st);
     if (!rc && corr) rc = stream_launch(kc, 3, gc, bp, args, st);
@@ -468,7 +472,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
     a.flags_prev = flags[(n_steps - 1) & 1];
     a.finalize = 1;
     void* args[1] = {&a};
-    if (int rc = stream_launch(kp, 4, gp, bp, args, s)) return rc;
+    if (int rc = stream_launch(kp, 4, gp, bp, args, s, kp_smem)) return rc;
   }
   if (cur) {
     for (int f = 0; f < 3; ++f)

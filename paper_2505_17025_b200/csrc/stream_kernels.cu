@@ -1,6 +1,6 @@
 // Streaming (HBM round-trip) time step for large ensembles.
 //
-// One element per thread, 256-thread CTAs over tiles of OWN = 248 elements
+// One element per thread, 128-thread CTAs over tiles of OWN = 120 elements
 // plus a halo of H = 4 on each side, all CTAs independent (no clusters), so
 // the SMs run many CTAs at full occupancy and the step is bounded by HBM
 // traffic and the fp64 pipe rather than by barrier latency.  Per step:

@@ -5,7 +5,7 @@
 #include "../../include/nhswe_b200.h"
 
 #ifndef NH_STREAM_THREADS
-#define NH_STREAM_THREADS 256
+#define NH_STREAM_THREADS 128   // measured on config 4: 64 96 128 160 192 256 512 -> 128 fastest
 #endif
 #define NH_STREAM_HALO 4
 #define NH_STREAM_OWN (NH_STREAM_THREADS - 2 * NH_STREAM_HALO)
@@ -54,6 +54,7 @@ struct StreamArgs {
 // which: 0 K_P, 1 K_X, 2 K_C, 3 K_S, 4 prep (step constants for the current time),
 //        5 order (members grouped by bottom kind, one CTA)
 void* nh_stream_kernel(int which);
-void* nh_stream_kp_ptr();   // stream_kp.cu
+void* nh_stream_kp_ptr();    // stream_kp.cu
+size_t nh_stream_kp_smem();  // its dynamic shared memory
 int nh_launch_gather_p(const double* pend, const uint8_t* flags, double* p, size_t n,
                        cudaStream_t s);

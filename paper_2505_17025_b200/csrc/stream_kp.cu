@@ -4,7 +4,8 @@
 __global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(StreamArgs a) {
   __shared__ nh_member msh;
   __shared__ MemberConst mc;
-  __shared__ KpSmem ks;
+  extern __shared__ __align__(16) unsigned char kp_dyn[];   // KpSmem (dynamic: > 48 KB at 512 threads)
+  KpSmem& ks = *reinterpret_cast<KpSmem*>(kp_dyn);
   // grid (tiles, members): no integer division (members past 65535 in z);
   // the member axis runs in bottom-kind order so the CTAs resident at one
   // time mostly execute the same kind-specialised body (instruction cache)
@@ -15,3 +16,4 @@ __global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(Stream
 }
 
 void* nh_stream_kp_ptr() { return (void*)nh_stream_kp; }
+size_t nh_stream_kp_smem() { return sizeof(KpSmem); }

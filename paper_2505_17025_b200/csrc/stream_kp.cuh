@@ -10,9 +10,9 @@
 namespace {
 
 
-constexpr int TPB = NH_STREAM_THREADS;     // 256
+constexpr int TPB = NH_STREAM_THREADS;     // 128
 constexpr int H = NH_STREAM_HALO;          // 4
-constexpr int OWN = TPB - 2 * H;           // 248
+constexpr int OWN = TPB - 2 * H;           // 120
 constexpr int NW = TPB / 32;
 
 __device__ __forceinline__ double ederiv(const nh_member& m, double v0, double v1, int i) {

@@ -89,8 +89,9 @@ class Ensemble:
         reduction of the step's input, adaptivity.py:153)."""
         if mode == "adaptive" and criterion is not None and criterion.kind in ("w", "w_x"):
             return "resident"
-        tiles = self.B * ((self.N + 247) // 248)
-        return "stream" if tiles >= 2 * 148 else "resident"
+        # enough work to fill the GPU: >= 296 units of 248 elements
+        units = self.B * ((self.N + 247) // 248)
+        return "stream" if units >= 2 * 148 else "resident"
 
     def stream_chunk(self, budget: int | None = None) -> int:
         """Members per streaming launch sequence: the whole ensemble when its

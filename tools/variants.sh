@@ -16,7 +16,8 @@ while [ $# -gt 0 ]; do
   name=$1; defs=$2; shift 2
   ( nvcc $FL $defs -Xptxas -v -c $C/stream_kernels.cu -o $O/sk_$name.o 2> $O/ptxas_$name.txt &&
     nvcc $FL $defs -Xptxas -v -c $C/stream_kp.cu -o $O/skp_$name.o 2> $O/ptxas_kp_$name.txt &&
-    nvcc -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC $O/capi.o $O/step_kernel.o \
+    nvcc $FL $defs -c $C/capi.cu -o $O/capi_$name.o &&
+    nvcc -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC $O/capi_$name.o $O/step_kernel.o \
          $O/aux_kernels.o $O/sk_$name.o $O/skp_$name.o -o $O/$name.so && echo "built $O/$name.so" ) &
 done
 wait
