@@ -403,6 +403,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   static const bool use_order = !getenv("NH_STREAM_ORDER") || atoi(getenv("NH_STREAM_ORDER")) != 0;
   a.order = use_order ? order : nullptr;
   const dim3 gp(T, std::min(B, 65535), (B + 65534) / 65535), bp(NH_STREAM_THREADS),
+      bpp(nh_stream_kp_threads()),
       gx((B + 7) / 8), bx(256);
   const dim3 gs((unsigned)std::min<size_t>(ks_grid, BT)), gc((unsigned)std::min<size_t>(kc_grid, BT));
   void* kp = nh_stream_kernel(0);
@@ -436,7 +437,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   auto launch_step = [&](int k, cudaStream_t st) -> int {
     set_step(k);
     void* args[1] = {&a};
-    int rc = stream_launch(kp, 0, gp, bp, args, st, kp_smem);
+    int rc = stream_launch(kp, 0, gp, bpp, args, st, kp_smem);
     if (!rc && corr) rc = stream_launch(ks, 1, gs, bp, args, st);
     if (!rc) rc = stream_launch(kx, 2, gx, bx, args, st);
     if (!rc && corr) rc = stream_launch(kc, 3, gc, bp, args, st);
@@ -472,7 +473,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
     a.flags_prev = flags[(n_steps - 1) & 1];
     a.finalize = 1;
     void* args[1] = {&a};
-    if (int rc = stream_launch(kp, 4, gp, bp, args, s, kp_smem)) return rc;
+    if (int rc = stream_launch(kp, 4, gp, bpp, args, s, kp_smem)) return rc;
   }
   if (cur) {
     for (int f = 0; f < 3; ++f)

@@ -20,7 +20,7 @@
 #define NH_KP_WARP_XCHG 0      // 1: K_P neighbour exchange by shuffles + warp-pair named barriers (measured slower)
 #endif
 #ifndef NH_KS_MIN_BLOCKS
-#define NH_KS_MIN_BLOCKS (768 / NH_STREAM_THREADS)        // K_S / K_C CTAs per SM
+#define NH_KS_MIN_BLOCKS (1024 / NH_STREAM_THREADS)       // K_S / K_C CTAs per SM (64 registers; measured 6 / 8 / 10 at 128 threads: 8 fastest)
 #endif
 
 struct StreamArgs {
@@ -56,5 +56,6 @@ struct StreamArgs {
 void* nh_stream_kernel(int which);
 void* nh_stream_kp_ptr();    // stream_kp.cu
 size_t nh_stream_kp_smem();  // its dynamic shared memory
+int nh_stream_kp_threads();  // its block size (NH_KP_E2: half a tile)
 int nh_launch_gather_p(const double* pend, const uint8_t* flags, double* p, size_t n,
                        cudaStream_t s);

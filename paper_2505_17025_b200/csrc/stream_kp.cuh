@@ -49,8 +49,8 @@ __device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q
   const int lane = i & 31, warp = i >> 5;
   Bottom6 b0 = bottom_eval_sp_k<KIND>(m, bt, x0, s0);
   Bottom6 b1 = bottom_eval_sp_k<KIND>(m, bt, x1, s1);
-  Side n0 = make_side(q.h0, q.q0, q.w0, b0.d);
-  Side n1 = make_side(q.h1, q.q1, q.w1, b1.d);
+  Side n0, n1;
+  make_sides_warp(q.h0, q.q0, q.w0, b0.d, q.h1, q.q1, q.w1, b1.d, n0, n1);
   // left neighbour's node-1 side (u included: no second division)
   Side L;
   L.h = __shfl_up_sync(0xffffffffu, n1.h, 1);
@@ -78,7 +78,7 @@ __device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q
   if (e == 0) L = ghost_side(n0, m.bc_left);
   // (CTA slot 0 keeps lane 0's own value: a halo element, never used)
   double sp;
-  Face fl = face_flux<KIND == NH_BOTTOM_FLAT>(L, n0, g, sp);
+  Face fl = face_flux<KIND == NH_BOTTOM_FLAT, true>(L, n0, g, sp);
   speed = fmax(speed, sp);
   Face fr;
   fr.F1 = __shfl_down_sync(0xffffffffu, fl.F1, 1);

@@ -4,7 +4,7 @@ perturbed by 1 ulp and run to the final step, recording the per-step flagged
 count.  Prints the full-run mask fraction mean of the perturbed trajectory
 (reference counts for steps <= S) next to the reference's own.
 
-    python tools/config3_perturbed.py [S] [element]  > profiles/r1_config3_perturbed.txt
+    python tools/config3_perturbed.py [S] [element] [rel]  > profiles/r1_config3_perturbed.txt
 """
 import os
 import sys
@@ -19,6 +19,7 @@ from tests.helpers import oracle_member  # noqa: E402
 
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
 E = int(sys.argv[2]) if len(sys.argv) > 2 else 1500
+REL = float(sys.argv[3]) if len(sys.argv) > 3 else 0.0   # 0: one ulp; else a relative kick of all h
 G = np.load(os.path.join(os.path.dirname(__file__), "..", "tests", "golden", "config3_full.npz"))
 cfg = configs.config3()
 m = cfg.member(0)
@@ -26,7 +27,11 @@ mem = oracle_member(m.grid, m.bathymetry, m.bcs, m.dt)
 r = G[f"ck/s{S}"]
 t = float(G[f"ck/t{S}"])
 h, hu, hw = r[0].copy(), r[1].copy(), r[2].copy()
-h[E, 0] = np.nextafter(h[E, 0], np.inf)
+if REL:
+    rng = np.random.default_rng(1)
+    h = h * (1.0 + REL * rng.standard_normal(h.shape))
+else:
+    h[E, 0] = np.nextafter(h[E, 0], np.inf)
 n = int(G["n_steps"])
 ref_counts = G["adaptive/flag_count"].astype(np.int64)
 counts = list(ref_counts[:S])
@@ -45,4 +50,4 @@ c = np.array(counts)
 print(f"final: mask fraction mean perturbed {c.mean() / m.grid.n_elements:.4f}, reference "
       f"{float(G['adaptive/mask_fraction']):.4f}; final eta max |.| perturbed "
       f"{np.abs(h - O.depth_of(mem, t) if hasattr(O, 'depth_of') else h).max():.4f}")
-np.save("/tmp/config3_perturbed_counts.npy", c)
+np.save(f"/tmp/config3_perturbed_counts_{S}_{E}_{REL:g}.npy", c)
