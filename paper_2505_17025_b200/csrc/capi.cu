@@ -412,6 +412,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   void* kc = nh_stream_kernel(2);
   void* ks = nh_stream_kernel(3);
   const bool corr = sc.mode != NH_MODE_HYDROSTATIC;
+  const bool fused_ks = nh_stream_kp_fuses_ks() != 0;
   {
     void* args[1] = {&a};
     if (int rc = stream_launch(nh_stream_kernel(4), 5, dim3((B + 255) / 256), dim3(256), args, s))
@@ -438,7 +439,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
     set_step(k);
     void* args[1] = {&a};
     int rc = stream_launch(kp, 0, gp, bpp, args, st, kp_smem);
-    if (!rc && corr) rc = stream_launch(ks, 1, gs, bp, args, st);
+    if (!rc && corr && !fused_ks) rc = stream_launch(ks, 1, gs, bp, args, st);
     if (!rc) rc = stream_launch(kx, 2, gx, bx, args, st);
     if (!rc && corr) rc = stream_launch(kc, 3, gc, bp, args, st);
     return rc;

@@ -24,12 +24,7 @@
 // applies the last pending hw update in place.
 #include "stream_kp.cuh"
 
-struct KsSmem {
-  double wnode[NW * 31 * 6];
-  double wagg[NW * 6];
-  double bnode[31 * 6];
-  int wflag[NW];
-};
+
 
 
 // ---------------------------------------------------------------------- K_S
@@ -48,37 +43,15 @@ __device__ __forceinline__ void ks_body(const StreamArgs& a, int bt, const nh_me
   const size_t o = ((size_t)b * N + (valid ? e : 0)) * 2;
   const size_t fe = (size_t)b * N + (valid ? e : 0);
   const bool flag = own && a.flags_cur[fe];
-  nh_status* st = a.status + b;
-  const int step = a.step_counter ? a.step_counter[b] : 0;
   Super S = super_identity();
   if (own) S = super_gap(a.hu_out[o]);
   if (flag) {
-    const double ed = (double)e;
-    const double x0 = sample_xd(m, ed, 0), x1 = sample_xd(m, ed, 1);
     double2 vh = *reinterpret_cast<const double2*>(a.h_out + o);
     double2 vq = *reinterpret_cast<const double2*>(a.hu_out + o);
     double2 vw = *reinterpret_cast<const double2*>(a.hw_out + o);
     const bool range_end = (e == N - 1) || !a.flags_cur[fe + 1];
-    Bottom6 b0 = bottom_eval<KIND, true>(m, bt1, x0);
-    Bottom6 b1 = bottom_eval<KIND, true>(m, bt1, x1);
-    Chan ch0{b0.d, b0.d_x, b0.d_t, b0.d_tt, b0.d_xt, b0.d_xx};
-    Chan ch1{b1.d, b1.d_x, b1.d_t, b1.d_tt, b1.d_xt, b1.d_xx};
-    double exa = ederiv(m, vh.x - b0.d, vh.y - b1.d, 0);
-    double exb = ederiv(m, vh.x - b0.d, vh.y - b1.d, 1);
-    NodeCoef c0 = ldg_coefficients(vh.x, vq.x, vw.x, ederiv(m, vh.x, vh.y, 0), exa, ch0, lk);
-    NodeCoef c1 = ldg_coefficients(vh.y, vq.y, vw.y, ederiv(m, vh.x, vh.y, 1), exb, ch1, lk);
-    double R[6];
-    if (!local_condense(m, c0, c1, lk.rho, lk.inv_rho, a.sch.c11, range_end, S, R))
-      nh_report(st, step, NH_ERR_SOLVE_PIVOT, e);
-    // field-major planes: each store of the warp is one coalesced 256-byte run
-    const size_t BN = (size_t)a.B * N;
-    double* sc = a.scratch + fe;
-    sc[0 * BN] = S.ga; sc[1 * BN] = S.aa; sc[2 * BN] = S.ba;
-    sc[3 * BN] = S.gz; sc[4 * BN] = S.az; sc[5 * BN] = S.bz;
-#pragma unroll
-    for (int r = 0; r < 6; ++r) sc[(6 + r) * BN] = R[r];
-    double* pn = a.pend_out + fe;
-    pn[2 * BN] = c0.phi; pn[3 * BN] = c1.phi; pn[4 * BN] = b0.d_x; pn[5 * BN] = b1.d_x;
+    condense_element<KIND>(a, m, lk, bt1, b, e, Q6{vh.x, vh.y, vq.x, vq.y, vw.x, vw.y},
+                           range_end, S);
   }
   Super v = tile_up(S, flag, ks.wnode, ks.wagg, ks.bnode, ks.wflag, lane, warp);
   if (i == 0) store_super(a.tile_agg + ((size_t)b * T + tile) * 8, v);

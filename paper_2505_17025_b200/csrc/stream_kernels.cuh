@@ -57,5 +57,6 @@ void* nh_stream_kernel(int which);
 void* nh_stream_kp_ptr();    // stream_kp.cu
 size_t nh_stream_kp_smem();  // its dynamic shared memory
 int nh_stream_kp_threads();  // its block size (NH_KP_E2: half a tile)
+int nh_stream_kp_fuses_ks(); // 1: K_P condenses its flagged tiles, no K_S launch
 int nh_launch_gather_p(const double* pend, const uint8_t* flags, double* p, size_t n,
                        cudaStream_t s);

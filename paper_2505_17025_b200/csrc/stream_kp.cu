@@ -43,3 +43,4 @@ int nh_stream_kp_threads() { return TPB; }
 #endif
 
 void* nh_stream_kp_ptr() { return (void*)nh_stream_kp; }
+int nh_stream_kp_fuses_ks() { return (NH_KP_FUSE_KS && !NH_KP_E2) ? 1 : 0; }

@@ -189,6 +189,11 @@ __device__ __forceinline__ Super tile_up(Super agg, bool tflag, double* wnode, d
 
 }  // namespace
 
+#ifndef NH_KP_FUSE_KS
+#define NH_KP_FUSE_KS 0   // 1: K_P also condenses its flagged tiles (no K_S launch); measured slower
+                          // (config 4 adaptive K_P+K_S 0.77 -> 0.86 ms: register pressure on every tile)
+#endif
+
 // ---------------------------------------------------------------------- K_P
 struct KpSmem {
 #if NH_KP_WARP_XCHG
@@ -206,6 +211,15 @@ struct KpSmem {
   uint8_t rf[TPB];
 };
 
+
+
+struct KsSmem {
+  double wnode[NW * 31 * 6];
+  double wagg[NW * 6];
+  double bnode[31 * 6];
+  int wflag[NW];
+};
+static_assert(sizeof(KsSmem) <= 12 * TPB * sizeof(double), "K_S tree nodes alias sk + sq");
 
 // Per-thread geometry of a streaming tile.
 struct TileIdx {
@@ -257,6 +271,40 @@ __device__ __forceinline__ void load_member(const StreamArgs& a, int b, nh_membe
   else if (i < MW + 16)
     reinterpret_cast<unsigned long long*>(&mc)[i - MW] =
         reinterpret_cast<const unsigned long long*>(a.mconst + (size_t)b * 16)[i - MW];
+}
+
+// One flagged element's LDG condensation (K_S, or K_P with NH_KP_FUSE_KS):
+// LDG coefficients at t + dt (corrector.py:100-170), the element block
+// eliminated to its super-element (corrector.py:173-349 -> physics.cuh), the
+// super-element + reconstruction rows stored for K_C, and phi / d_x stored in
+// the pending record of the hw update.  q = predictor state of the element.
+template <int KIND>
+__device__ __forceinline__ void condense_element(const StreamArgs& a, const nh_member& m,
+                                                 const LdgConst& lk, const BottomTime& bt1, int b,
+                                                 int e, const Q6& q, bool range_end, Super& S) {
+  const int N = a.N;
+  const double ed = (double)e;
+  const double x0 = sample_xd(m, ed, 0), x1 = sample_xd(m, ed, 1);
+  Bottom6 b0 = bottom_eval<KIND, true>(m, bt1, x0);
+  Bottom6 b1 = bottom_eval<KIND, true>(m, bt1, x1);
+  Chan ch0{b0.d, b0.d_x, b0.d_t, b0.d_tt, b0.d_xt, b0.d_xx};
+  Chan ch1{b1.d, b1.d_x, b1.d_t, b1.d_tt, b1.d_xt, b1.d_xx};
+  double exa = ederiv(m, q.h0 - b0.d, q.h1 - b1.d, 0);
+  double exb = ederiv(m, q.h0 - b0.d, q.h1 - b1.d, 1);
+  NodeCoef c0 = ldg_coefficients(q.h0, q.q0, q.w0, ederiv(m, q.h0, q.h1, 0), exa, ch0, lk);
+  NodeCoef c1 = ldg_coefficients(q.h1, q.q1, q.w1, ederiv(m, q.h0, q.h1, 1), exb, ch1, lk);
+  double R[6];
+  if (!local_condense(m, c0, c1, lk.rho, lk.inv_rho, a.sch.c11, range_end, S, R))
+    nh_report(a.status + b, a.step_counter ? a.step_counter[b] : 0, NH_ERR_SOLVE_PIVOT, e);
+  // field-major planes: each store of the warp is one coalesced run
+  const size_t BN = (size_t)a.B * N, fe = (size_t)b * N + e;
+  double* sc = a.scratch + fe;
+  sc[0 * BN] = S.ga; sc[1 * BN] = S.aa; sc[2 * BN] = S.ba;
+  sc[3 * BN] = S.gz; sc[4 * BN] = S.az; sc[5 * BN] = S.bz;
+#pragma unroll
+  for (int r = 0; r < 6; ++r) sc[(6 + r) * BN] = R[r];
+  double* pn = a.pend_out + fe;
+  pn[2 * BN] = c0.phi; pn[3 * BN] = c1.phi; pn[4 * BN] = b0.d_x; pn[5 * BN] = b1.d_x;
 }
 
 template <int KIND>
@@ -436,6 +484,17 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
         a.tile_list[atomicAdd(a.tile_count, 1)] = b * T + tile;   // work list of K_S / K_C
       }
     }
+#if NH_KP_FUSE_KS
+    if (nf) {   // CTA-uniform: this tile's condensation and aggregate (K_S's work)
+      Super S = super_identity();
+      if (own) S = super_gap(qp.q0);
+      if (flag) condense_element<KIND>(a, m, mc.lk, mc.bt1, b, e, qp, (e == N - 1) || !eff(i + 1), S);
+      // tree nodes in the k1 / step-start planes, dead since the Heun combination
+      KsSmem& kss = *reinterpret_cast<KsSmem*>(ks.sk);
+      Super v = tile_up(S, flag, kss.wnode, kss.wagg, kss.bnode, kss.wflag, lane, ti.warp);
+      if (i == 0) store_super(a.tile_agg + ((size_t)b * T + tile) * 8, v);
+    }
+#endif
     // right-end ghost outer trace (corrector.py:400-402)
     if (e == N - 1 && own) {
       double qq = qp.q1;
