@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define NH_ABI_VERSION 1
+#define NH_ABI_VERSION 2   /* 2: nh_outputs gauge fields */
 
 /* bottom model kinds (reference bathymetry.py:66-184 + harness models) */
 #define NH_BOTTOM_FLAT 0          /* FlatBottom(h0)                         bathymetry.py:66-79   */
@@ -115,6 +115,14 @@ typedef struct nh_outputs {
     uint32_t* flag_bits;    /* [n_steps][B][ceil(N/32)] per-step mask bits, or NULL */
     double* p_nh;           /* [B][N][2] pressure of the last step (0 off ranges), or NULL */
     const uint32_t* given_flags; /* NH_MODE_CORRECT_GIVEN: [B][ceil(N/32)] */
+    /* Gauges (driver.py:58-69, 88-94): h at n_gauges sample nodes after every
+     * step, recorded on the device so the loop never syncs.  gauge_nodes[g] =
+     * flat index e*2 + j of the node in a member's (N, 2) field; gauge_h is
+     * [n_steps][B][n_gauges].  The host subtracts the depth at the gauge's
+     * sample node and time, as the reference's record_gauges does. */
+    const int32_t* gauge_nodes;
+    double* gauge_h;
+    int32_t n_gauges;
 } nh_outputs;
 
 int nh_abi_version(void);

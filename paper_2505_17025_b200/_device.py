@@ -173,12 +173,21 @@ def scheme(mode: int, kind: str = "eta_over_d", k_nh: float = 1e-3, enlarge: boo
     return s
 
 
+def _outputs(flag_bits=None, p_out=None, given=None, gauges=None):
+    """nh_outputs; gauges = (int32 node indices [G], float64 out [n_steps][B][G]) or None."""
+    if gauges is None:
+        return _lib.Outputs(ptr(flag_bits), ptr(p_out), ptr(given), None, None, 0)
+    nodes, out = gauges
+    return _lib.Outputs(ptr(flag_bits), ptr(p_out), ptr(given), ptr(nodes), ptr(out),
+                        int(nodes.numel()))
+
+
 def advance(members, h, hu, hw, time, n_steps, sch, status, flag_bits=None, p_out=None,
-            given=None):
+            given=None, gauges=None):
     """Enqueue nh_advance (resident cluster kernel) on the current stream, in place."""
     lib = require_cuda()
     B, N = h.shape[0], h.shape[1]
-    out = _lib.Outputs(ptr(flag_bits), ptr(p_out), ptr(given))
+    out = _outputs(flag_bits, p_out, given, gauges)
     rc = lib.nh_advance(ptr(members), B, N, ptr(h), ptr(hu), ptr(hw), ptr(time), int(n_steps),
                         ctypes.byref(sch), ctypes.byref(out), ptr(status), stream_ptr())
     _lib.check(rc, "nh_advance")
@@ -191,11 +200,11 @@ def stream_workspace(B: int, N: int):
 
 
 def stream_advance(members, h, hu, hw, time, n_steps, sch, status, workspace, flag_bits=None,
-                   p_out=None):
+                   p_out=None, gauges=None):
     """Enqueue nh_stream_advance (tiled streaming kernels) on the current stream, in place."""
     lib = require_cuda()
     B, N = h.shape[0], h.shape[1]
-    out = _lib.Outputs(ptr(flag_bits), ptr(p_out), None)
+    out = _outputs(flag_bits, p_out, None, gauges)
     rc = lib.nh_stream_advance(ptr(members), B, N, ptr(h), ptr(hu), ptr(hw), ptr(time),
                                int(n_steps), ctypes.byref(sch), ctypes.byref(out), ptr(status),
                                ptr(workspace), workspace.numel(), stream_ptr())

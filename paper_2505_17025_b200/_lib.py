@@ -47,8 +47,11 @@ class Scheme(ctypes.Structure):
 
 class Outputs(ctypes.Structure):
     _fields_ = [("flag_bits", ctypes.c_void_p), ("p_nh", ctypes.c_void_p),
-                ("given_flags", ctypes.c_void_p)]
+                ("given_flags", ctypes.c_void_p), ("gauge_nodes", ctypes.c_void_p),
+                ("gauge_h", ctypes.c_void_p), ("n_gauges", ctypes.c_int32)]
 
+
+ABI_VERSION = 2   # include/nhswe_b200.h NH_ABI_VERSION
 
 EXPORTS = ("nh_abi_version", "nh_advance", "nh_stream_advance", "nh_stream_workspace_bytes",
            "nh_rhs", "nh_criterion", "nh_coefficients",
@@ -99,7 +102,7 @@ def load(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.nh_abi_version() != 1:
+    if lib.nh_abi_version() != ABI_VERSION:
         raise RuntimeError("ABI version mismatch")
     _lib = lib
     return lib

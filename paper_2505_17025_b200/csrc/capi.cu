@@ -197,11 +197,15 @@ int nh_advance(const nh_member* members, int n_members, int n_elements, double* 
   if (p.cluster > NH_MAX_CLUSTER) return NH_E_UNSUPPORTED;
   int rc = set_attrs();
   if (rc) return rc;
-  StepArgs a;
+  StepArgs a{};
   a.members = members;
   a.h = h; a.hu = hu; a.hw = hw; a.time = time;
   a.status = status;
   a.flag_bits = outputs ? outputs->flag_bits : nullptr;
+  if (outputs && outputs->n_gauges > 0) {
+    if (!outputs->gauge_nodes || !outputs->gauge_h) return NH_E_ARG;
+    a.gauge_nodes = outputs->gauge_nodes; a.gauge_h = outputs->gauge_h; a.n_gauges = outputs->n_gauges;
+  }
   a.p_out = outputs ? outputs->p_nh : nullptr;
   a.given = outputs ? outputs->given_flags : nullptr;
   a.sch = sc;
@@ -398,6 +402,10 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   a.members = members; a.time = time; a.status = status; a.step_counter = counter;
   a.scratch = scratch; a.tile_agg = tagg; a.tile_io = tio;
   a.flag_bits = outputs ? outputs->flag_bits : nullptr;
+  if (outputs && outputs->n_gauges > 0) {
+    if (!outputs->gauge_nodes || !outputs->gauge_h) return NH_E_ARG;
+    a.gauge_nodes = outputs->gauge_nodes; a.gauge_h = outputs->gauge_h; a.n_gauges = outputs->n_gauges;
+  }
   a.sch = sc; a.B = B; a.N = N; a.tiles = T; a.finalize = 0;
   a.tile_list = tlist; a.mconst = mconst;
   static const bool use_order = !getenv("NH_STREAM_ORDER") || atoi(getenv("NH_STREAM_ORDER")) != 0;
@@ -439,6 +447,9 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
     set_step(k);
     void* args[1] = {&a};
     int rc = stream_launch(kp, 0, gp, bpp, args, st, kp_smem);
+    if (!rc && a.n_gauges > 0)
+      rc = stream_launch(nh_stream_kernel(6), 5, dim3((unsigned)(((size_t)B * a.n_gauges + 127) / 128)),
+                         dim3(128), args, st);
     if (!rc && corr && !fused_ks) rc = stream_launch(ks, 1, gs, bp, args, st);
     if (!rc) rc = stream_launch(kx, 2, gx, bx, args, st);
     if (!rc && corr) rc = stream_launch(kc, 3, gc, bp, args, st);

@@ -532,6 +532,13 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
 
     // ---------------- step end: halo push, member-wide any(hw) ----------------
     __syncthreads();
+    // gauges: h is final once the predictor is done (the correction leaves it)
+    for (int gi = tid; gi < a.n_gauges; gi += T) {
+      const int node = a.gauge_nodes[gi], e = node >> 1;
+      if (e >= c0 && e < c1)
+        a.gauge_h[((size_t)step * a.B + b) * a.n_gauges + gi] =
+            fld(sm.Qn, S, F_H0 + (node & 1), e - c0 + H);
+    }
     NH_TS(7);
     if (C > 1) {
       const int per = H * 6;

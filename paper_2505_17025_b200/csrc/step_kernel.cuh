@@ -18,6 +18,9 @@ struct StepArgs {
   uint32_t* flag_bits;
   double* p_out;
   const uint32_t* given;
+  const int32_t* gauge_nodes;   // [n_gauges] flat node indices, or NULL
+  double* gauge_h;              // [n_steps][B][n_gauges]
+  int n_gauges;
   nh_scheme sch;
   int B, N, n_steps;
   int cluster, tile, nwords;

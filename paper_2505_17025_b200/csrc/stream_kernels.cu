@@ -133,6 +133,18 @@ __global__ void __launch_bounds__(256) nh_stream_prep(StreamArgs a) {
   if (b < a.B) member_const(a.members[b], a.sch, a.time[b], a.mconst + (size_t)b * 16);
 }
 
+// Gauges after K_P: h of this step (the correction leaves h unchanged) at
+// every gauge node of every member, into row step_counter[b] (K_X advances
+// it later in the step, so graph replays need no step argument).
+__global__ void __launch_bounds__(128) nh_stream_gauge(StreamArgs a) {
+  const size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (k >= (size_t)a.B * a.n_gauges) return;
+  const int b = (int)(k / a.n_gauges), gi = (int)(k % a.n_gauges);
+  const int step = a.step_counter[b];
+  a.gauge_h[((size_t)step * a.B + b) * a.n_gauges + gi] =
+      a.h_out[(size_t)b * a.N * 2 + a.gauge_nodes[gi]];
+}
+
 // Members grouped by bottom kind (stable within a kind), one 1024-thread CTA.
 __global__ void __launch_bounds__(1024) nh_stream_order(StreamArgs a) {
   __shared__ int wsum[32];
@@ -262,6 +274,7 @@ void* nh_stream_kernel(int which) {
     case 3: return (void*)nh_stream_ks;
     case 4: return (void*)nh_stream_prep;
     case 5: return (void*)nh_stream_order;
+    case 6: return (void*)nh_stream_gauge;
     default: return (void*)nh_stream_kc;
   }
 }

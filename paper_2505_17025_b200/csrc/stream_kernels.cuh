@@ -47,12 +47,15 @@ struct StreamArgs {
   int* tile_count;             // entries of tile_list (K_P appends, K_S / K_C consume)
   int* tile_count_next;        // the next step's counter, zeroed by K_X
   const int* order;            // [B] K_P's member order (grouped by bottom kind), or NULL
+  const int32_t* gauge_nodes;  // [n_gauges] flat node indices, or NULL
+  double* gauge_h;             // [n_steps][B][n_gauges]
+  int n_gauges;
   nh_scheme sch;
   int B, N, tiles, finalize;
 };
 
 // which: 0 K_P, 1 K_X, 2 K_C, 3 K_S, 4 prep (step constants for the current time),
-//        5 order (members grouped by bottom kind, one CTA)
+//        5 order (members grouped by bottom kind, one CTA), 6 gauges
 void* nh_stream_kernel(int which);
 void* nh_stream_kp_ptr();    // stream_kp.cu
 size_t nh_stream_kp_smem();  // its dynamic shared memory

@@ -108,8 +108,13 @@ class Ensemble:
 
     def advance(self, n_steps: int, mode: str = "adaptive", criterion: Criterion | None = None,
                 flux: FluxCoefficients = FluxCoefficients(), g: float = 9.81,
-                rho: float = RHO_WATER, flag_bits=None, p_out=None, path: str = "auto"):
-        """Enqueue n_steps time steps on the current stream (asynchronous)."""
+                rho: float = RHO_WATER, flag_bits=None, p_out=None, path: str = "auto",
+                gauges=None):
+        """Enqueue n_steps time steps on the current stream (asynchronous).
+
+        gauges = (int32 device tensor of flat node indices e*2 + j [G],
+        float64 device tensor [n_steps][B][G]) records h at those nodes after
+        every step on the device (reference driver.py:58-69)."""
         if mode not in _MODES:
             raise ValueError(f"unknown mode {mode!r}")
         if mode == "adaptive" and criterion is None:
@@ -124,12 +129,13 @@ class Ensemble:
                 self._ws = D.stream_workspace(chunk, self.N)
             if chunk >= self.B:
                 D.stream_advance(self.members, self.h, self.hu, self.hw, self.time, n_steps, sch,
-                                 self.status, self._ws, flag_bits, p_out)
+                                 self.status, self._ws, flag_bits, p_out, gauges)
                 return
             # members are independent: run the ensemble as consecutive member
             # blocks through one workspace (member-major state -> contiguous views)
-            if flag_bits is not None:
-                raise ValueError("per-step flag bits need the whole ensemble in one workspace")
+            if flag_bits is not None or gauges is not None:
+                raise ValueError("per-step flag bits and gauges need the whole ensemble in one "
+                                 "workspace")
             mb, sb = self.members, self.status
             rec, st = _lib.MEMBER_DTYPE.itemsize, _lib.STATUS_DTYPE.itemsize
             for c0 in range(0, self.B, chunk):
@@ -140,7 +146,7 @@ class Ensemble:
                                  None, None if p_out is None else p_out[c0:c1])
         else:
             D.advance(self.members, self.h, self.hu, self.hw, self.time, n_steps, sch,
-                      self.status, flag_bits, p_out)
+                      self.status, flag_bits, p_out, gauges=gauges)
 
     def check(self, t0=None):
         """Raise the reference exception for the first failed member, if any."""
@@ -185,23 +191,20 @@ def simulate(spec: ScenarioSpec, initial: FlowState, mode: str,
     ev0, ev1 = T.cuda.Event(enable_timing=True), T.cuda.Event(enable_timing=True)
     loop_ms = 0.0
     if n_steps > 0:
-        if not per_step:
-            ev0.record()
-            ens.advance(n_steps, mode, criterion, flux, spec.g, rho, bits, p)
-            ev1.record()
-            ev1.synchronize()
-            loop_ms = ev0.elapsed_time(ev1)
-        else:
-            ge = T.as_tensor([e for e, _ in gauge_idx], device="cuda")
-            gj = T.as_tensor([j for _, j in gauge_idx], device="cuda")
-            for s in range(n_steps):
-                ev0.record()
-                ens.advance(1, mode, criterion, flux, spec.g, rho,
-                            bits[s:s + 1] if bits is not None else None, p)
-                ev1.record()
-                ev1.synchronize()
-                loop_ms += ev0.elapsed_time(ev1)
-                gauge_h[s + 1] = ens.h[0, ge, gj].cpu().numpy()
+        # one launch sequence for the whole loop; gauges are recorded on the
+        # device after every step (no per-step synchronisation)
+        gauges = None
+        if per_step:
+            nodes = T.as_tensor([2 * e + j for e, j in gauge_idx], dtype=T.int32, device="cuda")
+            gauges = (nodes, T.empty((n_steps, 1, len(gauge_idx)), dtype=T.float64,
+                                     device="cuda"))
+        ev0.record()
+        ens.advance(n_steps, mode, criterion, flux, spec.g, rho, bits, p, gauges=gauges)
+        ev1.record()
+        ev1.synchronize()
+        loop_ms = ev0.elapsed_time(ev1)
+        if per_step:
+            gauge_h[1:] = gauges[1][:, 0, :].cpu().numpy()
     st = ens.check([initial.time])
     t = initial.time
     for s in range(n_steps):

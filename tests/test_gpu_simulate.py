@@ -205,3 +205,54 @@ def test_stream_graph_bitwise_equal_to_launches(n_steps, mode):
         D.stream_graphs(prev)
     for a, b in zip(out[0], out[1]):
         assert np.array_equal(a, b)
+
+
+def test_simulate_gauges_recorded_on_device():
+    """simulate() with gauges records h at the gauge nodes on the device every
+    step (one launch sequence, no per-step sync); gauge_eta matches the oracle
+    run step by step (reference driver.py:58-69, 88-94)."""
+    cfg = configs.config2()
+    m = cfg.member(0)
+    n_steps = 400
+    gauges = (0.05, 0.3, 0.31, 1.0, 2.5)
+    spec = P.ScenarioSpec("c2g", m.grid, m.dt, n_steps * m.dt, m.bathymetry, m.bcs, gauges)
+    h, hu, hw = cfg.host_state(0, oracle_depth)
+    init = P.FlowState(P.NodalField(m.grid, h), P.NodalField(m.grid, hu),
+                       P.NodalField(m.grid, hw), 0.0)
+    r = P.simulate(spec, init, "adaptive", P.Criterion("eta_over_d"))
+    mem = oracle_member(m.grid, m.bathymetry, m.bcs, m.dt)
+    idx = [m.grid.nearest_node(x) for x in gauges]
+    gx = np.array([m.grid.sample_nodes[e, j] for e, j in idx])
+    t = 0.0
+    ref = [h[tuple(np.array(idx).T)] - oracle_depth(m.bathymetry, gx, 0.0)]
+    for _ in range(n_steps):
+        o = O.step(mem, h, hu, hw, t, "adaptive", cfl_warn=False)
+        h, hu, hw = o.h, o.hu, o.hw
+        t = t + mem.dt
+        ref.append(h[tuple(np.array(idx).T)] - oracle_depth(m.bathymetry, gx, t))
+    ref = np.array(ref)
+    assert r.gauge_eta.shape == (n_steps + 1, len(gauges))
+    assert np.abs(r.gauge_eta - ref).max() <= 1e-12 * max(np.abs(ref).max(), 1e-6)
+    assert np.allclose(r.gauge_times[-1], n_steps * m.dt)
+
+
+@pytest.mark.parametrize("path", ["resident", "stream"])
+def test_ensemble_gauges_both_paths(path):
+    """Device gauge rows equal the state after each step, for every member, on
+    both paths (the stream path records them inside the CUDA-graph loop)."""
+    import torch
+    cfg = configs.Config4(n_members=6, n_elements=700, n_steps=9)
+    recs = cfg.records()
+    states = [cfg.host_state(i, oracle_depth) for i in range(cfg.n_members)]
+    H, Q, W = (np.stack([s[k] for s in states]) for k in range(3))
+    nodes = np.array([0, 1, 351, 700, 1398, 1399], dtype=np.int32)
+    ens = P.Ensemble.from_host(recs, H, Q, W)
+    ens_ref = P.Ensemble.from_host(recs, H, Q, W)
+    g = (torch.as_tensor(nodes, device="cuda"),
+         torch.full((cfg.n_steps, 6, nodes.size), np.nan, dtype=torch.float64, device="cuda"))
+    ens.advance(cfg.n_steps, "adaptive", P.Criterion("eta_over_d"), path=path, gauges=g)
+    out = g[1].cpu().numpy()
+    for s in range(cfg.n_steps):
+        ens_ref.advance(1, "adaptive", P.Criterion("eta_over_d"), path=path)
+        want = ens_ref.h.cpu().numpy().reshape(6, -1)[:, nodes]
+        assert np.array_equal(out[s], want), s
