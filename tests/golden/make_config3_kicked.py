@@ -1,10 +1,14 @@
-"""Config 3 chaos check (CPU, oracle = the reference's arithmetic bit for bit):
-restart the oracle from the reference's step-S checkpoint with one h value
-perturbed by 1 ulp and run to the final step, recording the per-step flagged
-count.  Prints the full-run mask fraction mean of the perturbed trajectory
-(reference counts for steps <= S) next to the reference's own.
+"""Config 3 sensitivity envelope (CPU; the oracle is the reference's
+arithmetic bit for bit, tests/test_oracle_golden.py): restart from the
+REFERENCE's own step-S checkpoint (config3_full.npz) with h perturbed -- one
+value by one ulp, or every value by a relative kick REL -- and run to the
+final step, recording the per-step flagged count.  With REL = 1e-10 at
+S = 20000 (the size of the GPU's drift there) this is the reference's own
+trajectory under a GPU-sized perturbation; tests/test_gpu_golden.py compares
+the GPU's full-run statistics with it.  Writes config3_kicked.npz next to
+this script (rel > 0 only).
 
-    python tools/config3_perturbed.py [S] [element] [rel]  > profiles/r1_config3_perturbed.txt
+    python tests/golden/make_config3_kicked.py [S] [element] [rel]
 """
 import os
 import sys
@@ -12,7 +16,7 @@ import time
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from oracle import nhswe_oracle as O  # noqa: E402
 from paper_2505_17025_b200 import configs  # noqa: E402
 from tests.helpers import oracle_member  # noqa: E402
@@ -20,7 +24,8 @@ from tests.helpers import oracle_member  # noqa: E402
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
 E = int(sys.argv[2]) if len(sys.argv) > 2 else 1500
 REL = float(sys.argv[3]) if len(sys.argv) > 3 else 0.0   # 0: one ulp; else a relative kick of all h
-G = np.load(os.path.join(os.path.dirname(__file__), "..", "tests", "golden", "config3_full.npz"))
+HERE = os.path.dirname(os.path.abspath(__file__))
+G = np.load(os.path.join(HERE, "config3_full.npz"))
 cfg = configs.config3()
 m = cfg.member(0)
 mem = oracle_member(m.grid, m.bathymetry, m.bcs, m.dt)
@@ -48,6 +53,8 @@ for k in range(S, n):
               f"({time.time() - t0:.0f}s)", flush=True)
 c = np.array(counts)
 print(f"final: mask fraction mean perturbed {c.mean() / m.grid.n_elements:.4f}, reference "
-      f"{float(G['adaptive/mask_fraction']):.4f}; final eta max |.| perturbed "
-      f"{np.abs(h - O.depth_of(mem, t) if hasattr(O, 'depth_of') else h).max():.4f}")
-np.save(f"/tmp/config3_perturbed_counts_{S}_{E}_{REL:g}.npy", c)
+      f"{float(G['adaptive/mask_fraction']):.4f}")
+if REL:
+    np.savez_compressed(os.path.join(HERE, "config3_kicked.npz"), start=np.array(S),
+                        rel=np.array(REL), counts=c.astype(np.int16),
+                        mask_fraction=np.array(c.mean() / m.grid.n_elements))

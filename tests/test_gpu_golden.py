@@ -106,12 +106,16 @@ LONG = [(c, m) for c in ("config1", "config2", "config3")
         for m in configs.get(c).modes]
 
 # Config 3's reference solution is dynamically sensitive after the slide stops
-# (t_stop = 1.96 s): in the reference's own arithmetic a 1-ulp perturbation of
-# h at step 15000 grows by orders of magnitude within 15000 more steps
-# (DESIGN.md §5), so no implementation that is not bitwise identical to LAPACK
-# can match it at t = 15 s.  Exact parity is gated on the reference
-# checkpoints through step 20000 (t = 2.66 s); the full run is compared on
-# its statistics.
+# (t_stop = 1.96 s).  The GPU's solve differs from LAPACK's by ~2e-14 per step
+# (one-step replay), its state drifts to ~1e-10 of the reference by step 20000,
+# and from step 34653 near-threshold mask flips put it on another trajectory.
+# The reference's OWN arithmetic does the same under a perturbation of that
+# size: restarted from its step-20000 checkpoint with h kicked by 1e-10
+# relative (tests/golden/make_config3_kicked.py, config3_kicked.npz) it ends
+# with a full-run mask fraction of 0.555 against its unperturbed 0.465 (the
+# GPU: 0.557).  Exact parity is gated on the reference checkpoints through
+# step 20000 (t = 2.66 s); the full run is compared with the envelope of the
+# reference and its kicked twin.
 CHAOTIC = {"config3": 20000}
 
 
@@ -165,7 +169,17 @@ def test_full_length_config_vs_reference(cfg_name, mode):
           f"GPU loop {res.loop_time:.3f}s vs reference {float(G[mode + '/loop_time']):.1f}s")
     if cfg_name in CHAOTIC:
         assert np.all(np.isfinite(res.final_state.hu.values))
-        assert abs(res.mask_fraction_mean - float(G[mode + "/mask_fraction"])) < 0.02
+        cnt = np.array([sum(e1 - e0 + 1 for e0, e1 in r) for _, _, r in res.mask_history])
+        exact = CHAOTIC[cfg_name]
+        # per-step flagged counts identical to the reference's through the gate
+        assert np.array_equal(cnt[:exact], G[mode + "/flag_count"][:exact])
+        K = np.load(os.path.join(GOLDEN, f"{cfg_name}_kicked.npz"))
+        lo = min(float(G[mode + "/mask_fraction"]), float(K["mask_fraction"]))
+        hi = max(float(G[mode + "/mask_fraction"]), float(K["mask_fraction"]))
+        print(f"{cfg_name}: mask fraction GPU {res.mask_fraction_mean:.4f}, reference "
+              f"{float(G[mode + '/mask_fraction']):.4f}, reference kicked by "
+              f"{float(K['rel']):.0e} at step {int(K['start'])}: {float(K['mask_fraction']):.4f}")
+        assert lo - 0.02 <= res.mask_fraction_mean <= hi + 0.02
         assert np.abs(eta).max() < 2 * np.abs(eta_ref).max()
         return
     assert e_eta <= 1e-9 and e_hu <= 1e-9

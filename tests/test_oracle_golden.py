@@ -2,6 +2,8 @@
 produced by tests/golden/make_golden.py from /root/reference) -- bit for bit on
 the host that made them; 1e-13 relative elsewhere (numpy/BLAS rounding)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -10,6 +12,7 @@ from tests.oracle_cases import NAMES, load_short, member_from, state_from
 
 D = load_short()
 TOL = 1e-13
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
 
 def close(a, b, tol=TOL):
@@ -89,3 +92,16 @@ def test_runs_helper():
     assert O.runs(np.array([], bool)) == ()
     assert O.runs(np.array([1, 1, 0, 1], bool)) == ((0, 1), (3, 3))
     assert O.runs(np.ones(4, bool)) == ((0, 3),)
+
+
+def test_config3_kicked_envelope_file():
+    """config3_kicked.npz (make_config3_kicked.py): the reference's arithmetic
+    restarted from its own step-20000 checkpoint with h kicked by 1e-10; its
+    counts equal the reference's up to the restart and it is a complete run."""
+    G = np.load(os.path.join(GOLDEN, "config3_full.npz"))
+    K = np.load(os.path.join(GOLDEN, "config3_kicked.npz"))
+    s = int(K["start"])
+    c = K["counts"].astype(np.int64)
+    assert c.size == int(G["n_steps"])
+    assert np.array_equal(c[:s], G["adaptive/flag_count"][:s])
+    assert abs(c.mean() / 8000 - float(K["mask_fraction"])) < 1e-12
