@@ -412,7 +412,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   a.order = use_order ? order : nullptr;
   const dim3 gp(T, std::min(B, 65535), (B + 65534) / 65535), bp(NH_STREAM_THREADS),
       bpp(nh_stream_kp_threads()),
-      gx((B + 7) / 8), bx(256);
+      gx((B + 7) / 8), bx(288);
   const dim3 gs((unsigned)std::min<size_t>(ks_grid, BT)), gc((unsigned)std::min<size_t>(kc_grid, BT));
   void* kp = nh_stream_kernel(0);
   const size_t kp_smem = nh_stream_kp_smem();

@@ -85,23 +85,41 @@ __global__ void __launch_bounds__(TPB, NH_KS_MIN_BLOCKS) nh_stream_ks(StreamArgs
 // One warp per member: chain of its T tile aggregates (lane l folds tiles
 // [l*cpl, (l+1)*cpl)), merge tree across lanes, back-substitution, then each
 // tile's (a_in, z_in).  Also advances the member's time and step counter.
-__global__ void __launch_bounds__(256) nh_stream_kx(StreamArgs a) {
+// 9 warps per CTA: warps 0-7 run the tile chains of 8 members; lanes 0-7 of
+// warp 8 advance the same 8 members' time and step constants concurrently.
+__global__ void __launch_bounds__(288) nh_stream_kx(StreamArgs a) {
   __shared__ double nodes[8][31 * 6];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.x * 8 + warp;
   if (blockIdx.x == 0 && threadIdx.x == 0 && a.tile_count_next) *a.tile_count_next = 0;
+  if (warp == 8) {
+    const int b = blockIdx.x * 8 + lane;
+    if (lane >= 8 || b >= a.B) return;
+    const nh_member& m = a.members[b];
+    const double tn = a.time[b] + m.dt;
+    a.time[b] = tn;
+    if (a.step_counter) a.step_counter[b] += 1;
+    // next step's constants: its bt0 = bottom_time(tn) is this step's bt1
+    // (the same call on the same argument, t + dt); only bt1 is new
+    MemberConst* mc = reinterpret_cast<MemberConst*>(a.mconst + (size_t)b * 16);
+    mc->bt0 = mc->bt1;
+    mc->bt1 = bottom_time(m, tn + m.dt);
+    return;
+  }
+  const int b = blockIdx.x * 8 + warp;
   if (b >= a.B) return;
   const int T = a.tiles;
   const int cpl = (T + 31) / 32;
   const double* ta = a.tile_agg + (size_t)b * T * 8;
-  bool any = false;
-  for (int k = lane; k < T; k += 32) any |= ta[k * 8 + 6] > 0.0;
-  any = __any_sync(0xffffffffu, any);
   double* io = a.tile_io + (size_t)b * T * 2;
-  if (any) {
-    Super agg = super_identity();
-    int k0 = lane * cpl, k1 = min(k0 + cpl, T);
-    for (int k = k0; k < k1; ++k) agg = merge2(agg, load_super(ta + k * 8));
+  // this lane's tiles: flagged counts and the folded aggregate in one pass
+  const int k0 = lane * cpl, k1 = min(k0 + cpl, T);
+  bool any = false;
+  Super agg = super_identity();
+  for (int k = k0; k < k1; ++k) {
+    any |= ta[k * 8 + 6] > 0.0;
+    agg = merge2(agg, load_super(ta + k * 8));
+  }
+  if (__any_sync(0xffffffffu, any)) {
     warp_up(agg, nodes[warp], lane, 5);
     double a_in = 0.0, z_in = ta[(T - 1) * 8 + 7];
     warp_down(a_in, z_in, nodes[warp], lane, 5);
@@ -118,12 +136,6 @@ __global__ void __launch_bounds__(256) nh_stream_kx(StreamArgs a) {
       z = fma(nv[k - k0], z, mv[k - k0]);
       io[k * 2 + 0] = fma(tv[k - k0], z, sv[k - k0]);
     }
-  }
-  if (lane == 0) {
-    const double tn = a.time[b] + a.members[b].dt;
-    a.time[b] = tn;
-    if (a.step_counter) a.step_counter[b] += 1;
-    member_const(a.members[b], a.sch, tn, a.mconst + (size_t)b * 16);   // next step's constants
   }
 }
 
