@@ -83,15 +83,16 @@ class Ensemble:
         self.status = D.new_status(self.B)
 
     def choose_path(self, mode: str, criterion: Criterion | None) -> str:
-        """Streaming tiles for ensembles that fill the GPU, the SMEM-resident
-        cluster kernel for small runs (lower per-step latency) and for the
-        w / w_x criteria (their first-step fallback needs a member-wide
-        reduction of the step's input, adaptivity.py:153)."""
+        """The streaming tiles with the CUDA-graph time loop for every run they
+        support -- measured faster than the SMEM-resident cluster kernel at
+        every size here, from one 200-element member (17 vs 22 us/step) to
+        config 3 (23 vs 47 us/step) and config 4 (0.83 vs 4.4 ms/step),
+        tools/scenario_paths.py, tools/path_compare.py -- and the resident
+        kernel for the w / w_x criteria, whose first-step fallback needs a
+        member-wide reduction of the step's input (adaptivity.py:153)."""
         if mode == "adaptive" and criterion is not None and criterion.kind in ("w", "w_x"):
             return "resident"
-        # enough work to fill the GPU: >= 296 units of 248 elements
-        units = self.B * ((self.N + 247) // 248)
-        return "stream" if units >= 2 * 148 else "resident"
+        return "stream"
 
     def stream_chunk(self, budget: int | None = None) -> int:
         """Members per streaming launch sequence: the whole ensemble when its
