@@ -5,6 +5,7 @@
 #include <atomic>
 #include <mutex>
 #include <vector>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include "step_kernel.cuh"
@@ -344,7 +345,7 @@ static int stream_tiles(int n) { return (n + NH_STREAM_OWN - 1) / NH_STREAM_OWN;
 size_t nh_stream_workspace_bytes(int n_members, int n_elements) {
   size_t BN = (size_t)n_members * n_elements, BT = (size_t)n_members * stream_tiles(n_elements);
   size_t dbl = 6 * BN + 12 * BN + 12 * BN + 10 * BT + 16 * (size_t)n_members;
-  return dbl * 8 + 2 * BN + 4 * (size_t)n_members + 8 + 4 * BT + 4 * (size_t)n_members + 1024;
+  return dbl * 8 + 2 * BN + 4 * (size_t)n_members + 8 + 4 * BT + 8 * (size_t)n_members + 1024;
 }
 
 int nh_stream_advance(const nh_member* members, int B, int N, double* h, double* hu, double* hw,
@@ -356,11 +357,10 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   if (workspace_bytes < nh_stream_workspace_bytes(B, N)) return NH_E_ARG;
   const nh_scheme& sc = *scheme;
   if (sc.mode < NH_MODE_HYDROSTATIC || sc.mode > NH_MODE_ADAPTIVE) return NH_E_UNSUPPORTED;
-  if (sc.mode == NH_MODE_ADAPTIVE && (sc.criterion == NH_CRIT_W || sc.criterion == NH_CRIT_W_X))
-    return NH_E_UNSUPPORTED;   // member-wide any(hw) fallback lives in the resident kernel
   if (sc.mode != NH_MODE_HYDROSTATIC && (sc.c12 != -0.5 || sc.c22 != 0.0)) return NH_E_UNSUPPORTED;
   const int T = stream_tiles(N);
   if ((T + 31) / 32 > NH_STREAM_MAXCPL) return NH_E_UNSUPPORTED;
+  if ((long long)B * T >= (1ll << 31)) return NH_E_UNSUPPORTED;   // tile ids are int
   if (n_steps == 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t BN = (size_t)B * N, BT = (size_t)B * T;
@@ -376,8 +376,13 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   int* tcount = counter + B;            // [2] flagged-tile counters (ping-pong by step)
   int* tlist = tcount + 2;              // [B*T] flagged-tile list
   int* order = tlist + BT;              // [B] K_P member order (by bottom kind)
+  int* hw_any = order + B;              // [B] w / w_x: any(hw != 0) of the step input (K_P -> K_F)
   if (cudaMemsetAsync(counter, 0, 4 * ((size_t)B + 2), s) != cudaSuccess) return NH_E_CUDA;
-  static int ks_grid = 0, kc_grid = 0;   // persistent grids: resident CTAs x SMs
+  const bool w_crit = sc.mode == NH_MODE_ADAPTIVE &&
+                      (sc.criterion == NH_CRIT_W || sc.criterion == NH_CRIT_W_X);
+  if (w_crit && !nh_stream_kp_records_hw_any()) return NH_E_UNSUPPORTED;
+  if (w_crit && cudaMemsetAsync(hw_any, 0, 4 * (size_t)B, s) != cudaSuccess) return NH_E_CUDA;
+  static int ks_grid = 0, kc_grid = 0, kp_pf_grid = 0;   // persistent grids: resident CTAs x SMs
   if (!ks_grid) {
     int dev = 0, sms = 0, nks = 0, nkc = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -390,6 +395,18 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
       return NH_E_CUDA;
     ks_grid = std::max(1, nks) * sms;
     kc_grid = std::max(1, nkc) * sms;
+    if (void* pf = nh_stream_kp_pf_ptr()) {   // persistent K_P: resident CTAs x SMs
+      int npf = 0;
+      if (cudaFuncSetAttribute(pf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)nh_stream_kp_pf_smem()) != cudaSuccess ||
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&npf, pf, NH_STREAM_THREADS,
+                                                        nh_stream_kp_pf_smem()) != cudaSuccess)
+        return NH_E_CUDA;
+      kp_pf_grid = std::max(1, npf) * sms;
+    }
+    if (getenv("NH_STREAM_VERBOSE"))
+      fprintf(stderr, "nh_stream: K_S grid %d, K_C grid %d, K_P persistent grid %d (smem %zu B)\n",
+              ks_grid, kc_grid, kp_pf_grid, nh_stream_kp_pf_smem());
     if (const char* v = getenv("NH_KS_WAVES")) {   // diagnostics: grid = waves x resident CTAs
       int wv = atoi(v);
       if (wv > 0) { ks_grid *= wv; kc_grid *= wv; }
@@ -408,6 +425,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   }
   a.sch = sc; a.B = B; a.N = N; a.tiles = T; a.finalize = 0;
   a.tile_list = tlist; a.mconst = mconst;
+  a.hw_any = w_crit ? hw_any : nullptr;
   static const bool use_order = !getenv("NH_STREAM_ORDER") || atoi(getenv("NH_STREAM_ORDER")) != 0;
   a.order = use_order ? order : nullptr;
   const dim3 gp(T, std::min(B, 65535), (B + 65534) / 65535), bp(NH_STREAM_THREADS),
@@ -416,6 +434,11 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   const dim3 gs((unsigned)std::min<size_t>(ks_grid, BT)), gc((unsigned)std::min<size_t>(kc_grid, BT));
   void* kp = nh_stream_kernel(0);
   const size_t kp_smem = nh_stream_kp_smem();
+  // the steps' K_P: the persistent prefetching kernel unless disabled (NH_KP_PF=0)
+  static const bool use_pf = !getenv("NH_KP_PF") || atoi(getenv("NH_KP_PF")) != 0;
+  void* kp_step = (use_pf && kp_pf_grid) ? nh_stream_kp_pf_ptr() : kp;
+  const dim3 gps = kp_step == kp ? gp : dim3((unsigned)std::min<size_t>(kp_pf_grid, BT));
+  const size_t kps_smem = kp_step == kp ? kp_smem : nh_stream_kp_pf_smem();
   void* kx = nh_stream_kernel(1);
   void* kc = nh_stream_kernel(2);
   void* ks = nh_stream_kernel(3);
@@ -446,10 +469,12 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   auto launch_step = [&](int k, cudaStream_t st) -> int {
     set_step(k);
     void* args[1] = {&a};
-    int rc = stream_launch(kp, 0, gp, bpp, args, st, kp_smem);
+    int rc = stream_launch(kp_step, 0, gps, bpp, args, st, kps_smem);
     if (!rc && a.n_gauges > 0)
       rc = stream_launch(nh_stream_kernel(6), 5, dim3((unsigned)(((size_t)B * a.n_gauges + 127) / 128)),
                          dim3(128), args, st);
+    if (!rc && w_crit)   // full mask for members whose input hw is identically zero
+      rc = stream_launch(nh_stream_kernel(7), 5, dim3((B + 7) / 8), dim3(256), args, st);
     if (!rc && corr && !fused_ks) rc = stream_launch(ks, 1, gs, bp, args, st);
     if (!rc) rc = stream_launch(kx, 2, gx, bx, args, st);
     if (!rc && corr) rc = stream_launch(kc, 3, gc, bp, args, st);

@@ -139,6 +139,45 @@ __global__ void __launch_bounds__(288) nh_stream_kx(StreamArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------- K_F
+// w / w_x criterion: a member whose step input has hw == 0 everywhere is
+// corrected globally for that step (adaptivity.py:153-154), so the indicator
+// can activate.  K_P flags by the criterion and records any(hw != 0) of the
+// input per member (hw_any); this kernel gives the all-zero members the full
+// mask before K_S: every element flagged (flags, flag bits, flagged count) and
+// every tile not yet on the work list appended to it.  One warp per member.
+__global__ void __launch_bounds__(256) nh_stream_kf(StreamArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * 8 + warp;
+  if (b >= a.B) return;
+  int any = 0;
+  if (lane == 0) {
+    any = a.hw_any[b];
+    a.hw_any[b] = 0;   // K_P of the next step records it afresh
+  }
+  if (__shfl_sync(0xffffffffu, any, 0)) return;
+  const int N = a.N, T = a.tiles;
+  double* ta = a.tile_agg + (size_t)b * T * 8;
+  unsigned long long had = 0;
+  for (int k = lane; k < T; k += 32) {
+    const double nf = ta[k * 8 + 6];
+    had += (unsigned long long)nf;
+    if (nf == 0.0) a.tile_list[atomicAdd(a.tile_count, 1)] = b * T + k;
+    ta[k * 8 + 6] = (double)min(OWN, N - k * OWN);
+  }
+  for (int o = 16; o > 0; o >>= 1) had += __shfl_xor_sync(0xffffffffu, had, o);
+  uint8_t* fl = a.flags_cur + (size_t)b * N;
+  for (int e = lane; e < N; e += 32) fl[e] = 1;
+  if (a.flag_bits) {
+    const int nw = (N + 31) / 32, step = a.step_counter ? a.step_counter[b] : 0;
+    uint32_t* fb = a.flag_bits + ((size_t)step * a.B + b) * nw;
+    for (int w = lane; w < nw; w += 32)
+      fb[w] = (w == nw - 1 && (N & 31)) ? ((1u << (N & 31)) - 1u) : 0xffffffffu;
+  }
+  if (lane == 0 && (unsigned long long)N > had)
+    atomicAdd((unsigned long long*)&a.status[b].flagged, (unsigned long long)N - had);
+}
+
 // Step constants of every member at its current time (before the first step).
 __global__ void __launch_bounds__(256) nh_stream_prep(StreamArgs a) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -287,6 +326,7 @@ void* nh_stream_kernel(int which) {
     case 4: return (void*)nh_stream_prep;
     case 5: return (void*)nh_stream_order;
     case 6: return (void*)nh_stream_gauge;
+    case 7: return (void*)nh_stream_kf;
     default: return (void*)nh_stream_kc;
   }
 }

@@ -49,17 +49,22 @@ struct StreamArgs {
   const int* order;            // [B] K_P's member order (grouped by bottom kind), or NULL
   const int32_t* gauge_nodes;  // [n_gauges] flat node indices, or NULL
   double* gauge_h;             // [n_steps][B][n_gauges]
+  int* hw_any;                 // [B] w / w_x criterion: any(hw != 0) of the step input, or NULL
   int n_gauges;
   nh_scheme sch;
   int B, N, tiles, finalize;
 };
 
 // which: 0 K_P, 1 K_X, 2 K_C, 3 K_S, 4 prep (step constants for the current time),
-//        5 order (members grouped by bottom kind, one CTA), 6 gauges
+//        5 order (members grouped by bottom kind, one CTA), 6 gauges,
+//        7 full-mask fallback of the w / w_x criteria (K_F)
 void* nh_stream_kernel(int which);
 void* nh_stream_kp_ptr();    // stream_kp.cu
 size_t nh_stream_kp_smem();  // its dynamic shared memory
 int nh_stream_kp_threads();  // its block size (NH_KP_E2: half a tile)
 int nh_stream_kp_fuses_ks(); // 1: K_P condenses its flagged tiles, no K_S launch
+int nh_stream_kp_records_hw_any();
+void* nh_stream_kp_pf_ptr();        // persistent prefetching K_P, or NULL (NH_KP_PERSIST=0)
+size_t nh_stream_kp_pf_smem();  // 1: K_P records any(hw != 0) for the w / w_x fallback
 int nh_launch_gather_p(const double* pend, const uint8_t* flags, double* p, size_t n,
                        cudaStream_t s);

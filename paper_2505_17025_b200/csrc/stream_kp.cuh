@@ -206,8 +206,8 @@ struct KpSmem {
   double sf[3 * TPB];
 #endif
   double sk[6 * TPB];     // k1 of this thread's element
-  double sq[6 * TPB];     // step-start state of this thread's element
-  double cfl;             // max wave speed of the tile (CFL = speed dt / dx at the end)
+  alignas(16) double sq[6 * TPB];   // step-start state: [3][TPB] double2 (h, hu, hw node pairs)
+  unsigned long long wcfl[NW];   // per warp: max wave speed bits (CFL = speed dt / dx at the end)
   uint8_t rf[TPB];
 };
 
@@ -307,10 +307,10 @@ __device__ __forceinline__ void condense_element(const StreamArgs& a, const nh_m
   pn[2 * BN] = c0.phi; pn[3 * BN] = c1.phi; pn[4 * BN] = b0.d_x; pn[5 * BN] = b1.d_x;
 }
 
-template <int KIND>
+template <int KIND, class SM>
 __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
                                         const MemberConst& mc, const TileIdx& ti, Q6 q,
-                                        KpSmem& ks) {
+                                        SM& ks, double* sq) {
   double* sh = ks.sh;
   double* sf = ks.sf;
   uint8_t* rf = ks.rf;
@@ -322,7 +322,6 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   double* XS = sh;
   double* XF = sf;
 #endif
-  double& cfl_sh = ks.cfl;
 
   const int N = a.N, T = a.tiles;
   const int b = ti.b, tile = ti.tile, i = ti.i, lane = ti.lane, e = ti.e;
@@ -342,8 +341,12 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   // ---------------- Heun stage 1 at t ----------------
   // positivity (hydrostatic.py:101-103, 216-217) gathered into one report
   unsigned bad = (own && (q.h0 <= 0.0 || q.h1 <= 0.0)) ? 1u : 0u;
-  ks.sq[0 * TPB + i] = q.h0; ks.sq[1 * TPB + i] = q.h1; ks.sq[2 * TPB + i] = q.q0;
-  ks.sq[3 * TPB + i] = q.q1; ks.sq[4 * TPB + i] = q.w0; ks.sq[5 * TPB + i] = q.w1;
+  {   // step-start state, one (node 0, node 1) pair per field: [3][TPB] double2
+    double2* s2 = reinterpret_cast<double2*>(sq);
+    s2[0 * TPB + i] = double2{q.h0, q.h1};
+    s2[1 * TPB + i] = double2{q.q0, q.q1};
+    s2[2 * TPB + i] = double2{q.w0, q.w1};
+  }
   Q6 qs;
   {
     double k1[6], dd0, dd1;
@@ -368,7 +371,8 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   double qv[6];
 #pragma unroll
   for (int f = 0; f < 6; ++f)
-    qv[f] = RADD(ks.sq[f * TPB + i], RMUL(dt, RMUL(0.5, RADD(ks.sk[f * TPB + i], k2[f]))));
+    qv[f] = RADD(sq[(f >> 1) * 2 * TPB + 2 * i + (f & 1)],
+                 RMUL(dt, RMUL(0.5, RADD(ks.sk[f * TPB + i], k2[f]))));
   Q6 qp{qv[0], qv[1], qv[2], qv[3], qv[4], qv[5]};
   bad |= (own && !(qp.h0 > 0.0 && qp.h1 > 0.0)) ? 4u : 0u;
   if (sch.record_cfl) {
@@ -378,8 +382,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
     const unsigned long long u = (unsigned long long)__double_as_longlong(own ? speed : 0.0);
     const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(u >> 32));
     const unsigned lo = __reduce_max_sync(0xffffffffu, (unsigned)(u >> 32) == hi ? (unsigned)u : 0u);
-    if (lane == 0 && (hi | lo))
-      atomicMax((unsigned long long*)&cfl_sh, ((unsigned long long)hi << 32) | lo);
+    if (lane == 0) ks.wcfl[ti.warp] = ((unsigned long long)hi << 32) | lo;
   }
 
   // ---------------- criterion on the predictor (t + dt) ----------------
@@ -444,8 +447,13 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   }
   // CFL of the tile = (max speed) dt / dx: rounding is monotone, so this is
   // the max over elements of the per-element speed dt / dx (hydrostatic.py CFL check)
-  auto publish_cfl = [&]() {
-    if (i == 0 && cfl_sh > 0.0) {
+  auto publish_cfl = [&]() {   // after the flags barrier: every warp's slot is written
+    if (i != 0 || !sch.record_cfl) return;
+    unsigned long long mx = ks.wcfl[0];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) mx = max(mx, ks.wcfl[w]);
+    const double cfl_sh = __longlong_as_double((long long)mx);
+    if (cfl_sh > 0.0) {
       const double c = cfl_sh * dt / m.dx;
       atomicMax((unsigned long long*)&st->cfl_max, (unsigned long long)__double_as_longlong(c));
     }
@@ -504,39 +512,19 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   publish_cfl();
 }
 
-// One K_P tile (b, tile): the body of nh_stream_kp.
-__device__ __forceinline__ void kp_tile(const StreamArgs& a, const TileIdx& ti, nh_member& msh,
-                                        MemberConst& mc, KpSmem& ks) {
+// The previous step's pending hw correction of the thread's element (q.w
+// updated in place) and the step body.  On entry the (h p) traces are in
+// ks.sh, made visible by the caller's barrier.
+// hw += dt/rho (6/quad p + d_x/quad (h p)_x + phi) on flagged elements
+// (corrector.py:441-482); (h p)_x lifts use the neighbours' (h p) traces.
+template <class SM>
+__device__ __forceinline__ void kp_correct_and_step(const StreamArgs& a, const TileIdx& ti,
+                                                    const nh_member& msh, const MemberConst& mc,
+                                                    SM& ks, double* sq, Q6 q, bool f, double p0,
+                                                    double p1, double phi0, double phi1,
+                                                    double dx0, double dx1) {
   const int N = a.N, i = ti.i, b = ti.b, e = ti.e;
-
-  // state and the previous step's pending record are requested first so their
-  // latency overlaps the member-record copy and the per-CTA constants
-  Q6 q{1.0, 1.0, 0.0, 0.0, 0.0, 0.0};
-  if (ti.valid) {
-    double2 vh = *reinterpret_cast<const double2*>(a.h_in + ti.o);
-    double2 vq = *reinterpret_cast<const double2*>(a.hu_in + ti.o);
-    double2 vw = *reinterpret_cast<const double2*>(a.hw_in + ti.o);
-    q = Q6{vh.x, vh.y, vq.x, vq.y, vw.x, vw.y};
-  }
-  const bool f = a.pend && ti.valid && a.flags_prev[(size_t)b * N + e];
-  double p0 = 0.0, p1 = 0.0, phi0 = 0.0, phi1 = 0.0, dx0 = 0.0, dx1 = 0.0;
-  if (f) {
-    const size_t BN = (size_t)a.B * N;
-    const double* pv = a.pend + (size_t)b * N + e;
-    p0 = pv[0]; p1 = pv[BN]; phi0 = pv[2 * BN]; phi1 = pv[3 * BN]; dx0 = pv[4 * BN]; dx1 = pv[5 * BN];
-  }
-  load_member(a, b, msh, mc);
   const double hp0 = q.h0 * p0, hp1 = q.h1 * p1;
-  if (a.pend) {
-    ks.sh[0 * TPB + i] = hp0;
-    ks.sh[1 * TPB + i] = hp1;
-  }
-  if (i == 0) ks.cfl = 0.0;
-  __syncthreads();
-
-  // ---------------- pending correction of the previous step ----------------
-  // hw += dt/rho (6/quad p + d_x/quad (h p)_x + phi) on flagged elements
-  // (corrector.py:441-482); (h p)_x lifts use the neighbours' (h p) traces.
   double bp0 = 0.0, bp1 = 0.0;
   if (f) {
     const double* sh = ks.sh;
@@ -576,16 +564,138 @@ __device__ __forceinline__ void kp_tile(const StreamArgs& a, const TileIdx& ti, 
     }
     return;
   }
+  if (a.hw_any) {   // w / w_x criterion: member-wide any(hw != 0) of the step input
+    if (__syncthreads_or(ti.own && (q.w0 != 0.0 || q.w1 != 0.0)) && i == 0) a.hw_any[b] = 1;
+  }
 #if NH_KP_RUNTIME_KIND
-  kp_body<-1>(a, msh, mc, ti, q, ks);
+  kp_body<-1>(a, msh, mc, ti, q, ks, sq);
 #else
   switch (msh.bottom_kind) {
-    case NH_BOTTOM_FLAT: kp_body<NH_BOTTOM_FLAT>(a, msh, mc, ti, q, ks); break;
-    case NH_BOTTOM_PLATE: kp_body<NH_BOTTOM_PLATE>(a, msh, mc, ti, q, ks); break;
-    case NH_BOTTOM_QUARTIC_SLIDE: kp_body<NH_BOTTOM_QUARTIC_SLIDE>(a, msh, mc, ti, q, ks); break;
-    case NH_BOTTOM_SMOOTH_BOX: kp_body<NH_BOTTOM_SMOOTH_BOX>(a, msh, mc, ti, q, ks); break;
-    default: kp_body<NH_BOTTOM_SLOPE_SLIDE>(a, msh, mc, ti, q, ks); break;
+    case NH_BOTTOM_FLAT: kp_body<NH_BOTTOM_FLAT>(a, msh, mc, ti, q, ks, sq); break;
+    case NH_BOTTOM_PLATE: kp_body<NH_BOTTOM_PLATE>(a, msh, mc, ti, q, ks, sq); break;
+    case NH_BOTTOM_QUARTIC_SLIDE: kp_body<NH_BOTTOM_QUARTIC_SLIDE>(a, msh, mc, ti, q, ks, sq); break;
+    case NH_BOTTOM_SMOOTH_BOX: kp_body<NH_BOTTOM_SMOOTH_BOX>(a, msh, mc, ti, q, ks, sq); break;
+    default: kp_body<NH_BOTTOM_SLOPE_SLIDE>(a, msh, mc, ti, q, ks, sq); break;
   }
 #endif
 }
 
+// One K_P tile (b, tile): the body of nh_stream_kp.
+__device__ __forceinline__ void kp_tile(const StreamArgs& a, const TileIdx& ti, nh_member& msh,
+                                        MemberConst& mc, KpSmem& ks) {
+  const int N = a.N, i = ti.i, b = ti.b, e = ti.e;
+
+  // state and the previous step's pending record are requested first so their
+  // latency overlaps the member-record copy and the per-CTA constants
+  Q6 q{1.0, 1.0, 0.0, 0.0, 0.0, 0.0};
+  if (ti.valid) {
+    double2 vh = *reinterpret_cast<const double2*>(a.h_in + ti.o);
+    double2 vq = *reinterpret_cast<const double2*>(a.hu_in + ti.o);
+    double2 vw = *reinterpret_cast<const double2*>(a.hw_in + ti.o);
+    q = Q6{vh.x, vh.y, vq.x, vq.y, vw.x, vw.y};
+  }
+  const bool f = a.pend && ti.valid && a.flags_prev[(size_t)b * N + e];
+  double p0 = 0.0, p1 = 0.0, phi0 = 0.0, phi1 = 0.0, dx0 = 0.0, dx1 = 0.0;
+  if (f) {
+    const size_t BN = (size_t)a.B * N;
+    const double* pv = a.pend + (size_t)b * N + e;
+    p0 = pv[0]; p1 = pv[BN]; phi0 = pv[2 * BN]; phi1 = pv[3 * BN]; dx0 = pv[4 * BN]; dx1 = pv[5 * BN];
+  }
+  load_member(a, b, msh, mc);
+  if (a.pend) {
+    ks.sh[0 * TPB + i] = q.h0 * p0;
+    ks.sh[1 * TPB + i] = q.h1 * p1;
+  }
+  __syncthreads();
+  kp_correct_and_step(a, ti, msh, mc, ks, ks.sq, q, f, p0, p1, phi0, phi1, dx0, dx1);
+}
+
+// ------------------------------------------------- K_P, persistent + prefetch
+// A persistent grid (resident CTAs x SMs) strides over the (member, tile)
+// list; while a CTA computes tile L it has the state and member record of
+// its next tile L + G in flight into the other shared-memory stage
+// (cp.async), the next tile's pending flags and the member index of the tile
+// after that in registers.  The stage of the tile being computed doubles as
+// its step-start copy (sq), so the two stages cost one state plane set more
+// than KpSmem.
+struct __align__(16) KpStage {
+  double q[6 * TPB];   // [3][TPB] double2: (h0, h1), (hu0, hu1), (hw0, hw1)
+  nh_member m;
+  MemberConst mc;
+};
+struct __align__(16) KpSmemP {
+  double sh[5 * TPB];
+  double sf[3 * TPB];
+  double sk[6 * TPB];
+  unsigned long long wcfl[NW];
+  uint8_t rf[TPB];
+  KpStage st[2];
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// issue the copies of tile (b, tile) into stage st (every thread its element;
+// threads 0..54 one word of the member record / step constants each)
+__device__ __forceinline__ void kp_prefetch(const StreamArgs& a, int b, int tile, KpStage& st) {
+  constexpr int MW = (int)(sizeof(nh_member) / 8);
+  const int i = threadIdx.x;
+  const int e = tile * OWN - H + i;
+  if (e >= 0 && e < a.N) {
+    const size_t o = ((size_t)b * a.N + e) * 2;
+    cp_async16(&st.q[0 * TPB + 2 * i], a.h_in + o);
+    cp_async16(&st.q[2 * TPB + 2 * i], a.hu_in + o);
+    cp_async16(&st.q[4 * TPB + 2 * i], a.hw_in + o);
+  } else {   // outside the domain: the defaults of kp_tile
+    double2* s2 = reinterpret_cast<double2*>(st.q);
+    s2[0 * TPB + i] = double2{1.0, 1.0};
+    s2[1 * TPB + i] = double2{0.0, 0.0};
+    s2[2 * TPB + i] = double2{0.0, 0.0};
+  }
+  if (i < MW)
+    cp_async8(reinterpret_cast<unsigned long long*>(&st.m) + i,
+              reinterpret_cast<const unsigned long long*>(a.members + b) + i);
+  else if (i < MW + 16)
+    cp_async8(reinterpret_cast<unsigned long long*>(&st.mc) + (i - MW),
+              reinterpret_cast<const unsigned long long*>(a.mconst + (size_t)b * 16) + (i - MW));
+  cp_async_commit();
+}
+
+// the raw pending-flag byte of the thread's element of tile (b, tile), loaded
+// from a clamped address so the load can stay in flight until the next tile
+// (validity and a.pend are applied where it is consumed)
+__device__ __forceinline__ uint8_t kp_pending_flag(const StreamArgs& a, int b, int tile) {
+  const int e = tile * OWN - H + (int)threadIdx.x;
+  const int ec = min(max(e, 0), a.N - 1);
+  return a.flags_prev[(size_t)b * a.N + ec];
+}
+
+// tile L of the stage st (its copies complete and visible), f = its pending flag
+__device__ __forceinline__ void kp_tile_staged(const StreamArgs& a, const TileIdx& ti,
+                                               KpStage& st, KpSmemP& ks, uint8_t fraw) {
+  const bool f = a.pend && ti.valid && fraw;
+  const int N = a.N, i = ti.i, b = ti.b, e = ti.e;
+  const double2* s2 = reinterpret_cast<const double2*>(st.q);
+  const double2 vh = s2[0 * TPB + i], vq = s2[1 * TPB + i], vw = s2[2 * TPB + i];
+  Q6 q{vh.x, vh.y, vq.x, vq.y, vw.x, vw.y};
+  double p0 = 0.0, p1 = 0.0, phi0 = 0.0, phi1 = 0.0, dx0 = 0.0, dx1 = 0.0;
+  if (f) {
+    const size_t BN = (size_t)a.B * N;
+    const double* pv = a.pend + (size_t)b * N + e;
+    p0 = pv[0]; p1 = pv[BN]; phi0 = pv[2 * BN]; phi1 = pv[3 * BN]; dx0 = pv[4 * BN]; dx1 = pv[5 * BN];
+  }
+  if (a.pend) {
+    ks.sh[0 * TPB + i] = q.h0 * p0;
+    ks.sh[1 * TPB + i] = q.h1 * p1;
+  }
+  __syncthreads();
+  kp_correct_and_step(a, ti, st.m, st.mc, ks, st.q, q, f, p0, p1, phi0, phi1, dx0, dx1);
+}

@@ -1,10 +1,11 @@
 """Time loop entry points (reference driver.py:50-103) and the batched API.
 
-``simulate`` keeps the reference signature.  The whole fixed-dt loop is ONE
-launch of the fused step kernel: the member stays resident in shared memory
-across all steps and its state crosses HBM once in and once out.
-``loop_time`` is device time (CUDA events) of the stepping launches, the
-analogue of the reference's loop-only perf_counter.
+``simulate`` keeps the reference signature.  The whole fixed-dt loop is one
+launch sequence of the streaming step kernels (a CUDA graph of step pairs,
+DESIGN.md §4.1), with gauges and flag bits recorded on the device, so there
+is no per-step host synchronisation.  ``loop_time`` is device time (CUDA
+events) of the stepping launches, the analogue of the reference's loop-only
+perf_counter.
 
 ``Ensemble`` / ``simulate_ensemble`` are the batched extension (SURVEY.md
 §8(b)): B independent channels of equal N with per-member grids, dt, bottoms
@@ -83,15 +84,13 @@ class Ensemble:
         self.status = D.new_status(self.B)
 
     def choose_path(self, mode: str, criterion: Criterion | None) -> str:
-        """The streaming tiles with the CUDA-graph time loop for every run they
-        support -- measured faster than the SMEM-resident cluster kernel at
-        every size here, from one 200-element member (17 vs 22 us/step) to
-        config 3 (23 vs 47 us/step) and config 4 (0.83 vs 4.4 ms/step),
-        tools/scenario_paths.py, tools/path_compare.py -- and the resident
-        kernel for the w / w_x criteria, whose first-step fallback needs a
-        member-wide reduction of the step's input (adaptivity.py:153)."""
-        if mode == "adaptive" and criterion is not None and criterion.kind in ("w", "w_x"):
-            return "resident"
+        """The streaming tiles with the CUDA-graph time loop: measured faster
+        than the SMEM-resident cluster kernel at every size here, from one
+        200-element member (17 vs 22 us/step) to config 3 (23 vs 47 us/step)
+        and config 4 (0.83 vs 4.4 ms/step), tools/scenario_paths.py,
+        tools/path_compare.py.  Every mode and criterion runs on it (the w /
+        w_x first-step fallback of adaptivity.py:153 is K_F); the resident
+        kernel stays available as path="resident"."""
         return "stream"
 
     def stream_chunk(self, budget: int | None = None) -> int:

@@ -256,3 +256,50 @@ def test_ensemble_gauges_both_paths(path):
         ens_ref.advance(1, "adaptive", P.Criterion("eta_over_d"), path=path)
         want = ens_ref.h.cpu().numpy().reshape(6, -1)[:, nodes]
         assert np.array_equal(out[s], want), s
+
+
+@pytest.mark.parametrize("kind,enlarge", [("w", False), ("w_x", False), ("w_x", True)])
+def test_w_criteria_stream_fallback(kind, enlarge):
+    """w / w_x criteria on the streaming path: a member whose step input has
+    hw == 0 everywhere is corrected globally for that step (adaptivity.py:
+    153-154; K_F).  Box uplifts start from rest (fallback on the first step
+    only), solitary members carry hw from the start (never), and so does a
+    still-water member after its first (roundoff-level) correction.  Per-step flags equal the
+    resident kernel's, final states match the oracle run."""
+    from paper_2505_17025_b200 import _device as D
+    cfg = configs.Config4(n_members=6, n_elements=512, n_steps=40)
+    n = cfg.n_steps
+    recs = [cfg.records()]
+    states = [cfg.host_state(i, oracle_depth) for i in range(cfg.n_members)]
+    members = [(m.grid, m.bathymetry, m.bcs, m.dt) for m in map(cfg.member, range(cfg.n_members))]
+    still = (P.GridSpec(0.0, 100.0, 512), P.FlatBottom(1.0), P.BoundaryPair(P.WALL, P.ABSORBING),
+             0.01)   # CFL 0.16
+    recs.append(D.member_record(*still))
+    members.append(still)
+    states.append((np.ones((512, 2)), np.zeros((512, 2)), np.zeros((512, 2))))
+    recs = np.concatenate(recs)
+    H, Q, W = (np.stack([s[k] for s in states]) for k in range(3))
+    B, nw = len(members), (512 + 31) // 32
+    crit = P.Criterion(kind, 1e-3, enlarge)
+    out = {}
+    for path in ("resident", "stream"):
+        ens = P.Ensemble.from_host(recs, H, Q, W)
+        bits = D.torch().zeros((n, B, nw), dtype=D.torch().int32, device="cuda")
+        ens.advance(n, "adaptive", crit, flag_bits=bits, path=path)
+        st = ens.check()
+        out[path] = (ens.h.cpu().numpy(), ens.hu.cpu().numpy(), ens.hw.cpu().numpy(),
+                     bits.cpu().numpy(), st["flagged"].copy())
+    assert np.array_equal(out["stream"][3], out["resident"][3])
+    assert np.array_equal(out["stream"][4], out["resident"][4])
+    first = out["stream"][3][0].view(np.uint32)       # step 0: input hw == 0 -> full mask
+    for i in range(B):
+        assert (first[i] == 0xFFFFFFFF).all() == (not np.any(W[i])), i
+    gh, gq, gw = out["stream"][:3]
+    for i, (grid, bathy, bcs, dt) in enumerate(members):
+        r = O.run(oracle_member(grid, bathy, bcs, dt), H[i], Q[i], W[i], n, mode="adaptive",
+                  kind=kind, enlarge=enlarge)
+        d = oracle_depth(bathy, grid.sample_nodes, r.t)
+        assert rel(gh[i] - d, r.h - d) <= 1e-9 or np.abs(gh[i] - r.h).max() <= 1e-15, i
+        assert np.abs(gq[i] - r.hu).max() <= 1e-9 * max(np.abs(r.hu).max(), 1e-12), i
+        assert np.abs(gw[i] - r.hw).max() <= 1e-9 * max(np.abs(r.hw).max(), 1e-12), i
+        assert abs(out["stream"][4][i] / (n * 512) - r.fraction_mean) < 1e-12, i

@@ -87,6 +87,6 @@ def test_ensemble_time_ratios_rows():
     assert rows[0]["mask_fraction"] == 1.0
     for r in rows[1:]:
         assert 0.0 <= r["mask_fraction"] <= 1.0 and r["ms_per_step"] > 0.0
-        assert r["path"] == ("resident" if r["criterion"] in ("w", "w_x") else "stream")
+        assert r["path"] == "stream"
     # the initial state is left untouched for the next variant
     assert np.array_equal(H.cpu().numpy(), np.stack([s[0] for s in st]))
