@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define NH_ABI_VERSION 2   /* 2: nh_outputs gauge fields */
+#define NH_ABI_VERSION 3   /* 2: nh_outputs gauge fields; 3: nh_pm_* (orders p > 1), w / w_x on nh_stream_advance */
 
 /* bottom model kinds (reference bathymetry.py:66-184 + harness models) */
 #define NH_BOTTOM_FLAT 0          /* FlatBottom(h0)                         bathymetry.py:66-79   */
@@ -184,6 +184,51 @@ long long nh_launch_count(void);
  * accumulated. */
 int nh_selftest_arith(long long n, unsigned long long seed, unsigned long long* mismatches,
                       void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Polynomial orders p = 1..3 (m = p + 1 <= 4 GLL nodes per element; SURVEY.md
+ * §8(f)4).  The reference grid and LDG templates are generic in m
+ * (grid.py:19-114, corrector.py:173-370); these entry points run the same
+ * step for any m with element-parallel kernels (csrc/pm_kernels.cu).  State
+ * fields are [B][N][m].  Per-member m-node operators come in nh_pm_member
+ * (the reference GridSpec's values, copied not recomputed); the nh_member
+ * record supplies x_left, dx, dt, eps, 2/dx, bottom and boundaries (its P1
+ * operator arrays are unused here).
+ * ------------------------------------------------------------------------- */
+#define NH_PM_MAX_NODES 4
+typedef struct nh_pm_member {
+    double weak_div[16];    /* M^-1 K, row-major m x m (leading dimension m) */
+    double lift_left[4];    /* M^-1 e_first                                  */
+    double lift_right[4];   /* M^-1 e_last                                   */
+    double mass[16];        /* dx/2 * reference mass, row-major m x m       */
+    double stiffness[16];   /* K[i][j] = int phi_i' phi_j (reference)       */
+    double deriv_ref[16];   /* GLL differentiation matrix                   */
+    double node_off[4];     /* 0.5*dx*(ref_j + 1): node j = x_left + dx*e + node_off[j] */
+} nh_pm_member;
+
+/* Workspace of nh_pm_advance in bytes. */
+size_t nh_pm_workspace_bytes(int m, int n_members, int n_elements);
+
+/* nh_advance for m nodes per element (modes HYDROSTATIC / GLOBAL / ADAPTIVE,
+ * every criterion, alternating LDG flux; outputs flag_bits, p_nh [B][N][m],
+ * gauges with flat node index e*m + j).  Per step: two Heun-stage kernels,
+ * then flags, per-element LDG condensation, one chain thread per member,
+ * reconstruction and the hw correction. */
+int nh_pm_advance(const nh_member* members, const nh_pm_member* pm, int m,
+                  int n_members, int n_elements, double* h, double* hu, double* hw,
+                  double* time, int n_steps, const nh_scheme* scheme,
+                  const nh_outputs* outputs, nh_status* status, void* workspace,
+                  size_t workspace_bytes, void* stream);
+
+/* rhs_operator (hydrostatic.py:88-184) and criterion_values
+ * (adaptivity.py:75-96) for m nodes per element; fields [B][N][m]. */
+int nh_pm_rhs(const nh_member* members, const nh_pm_member* pm, int m, int n_members,
+              int n_elements, const double* h, const double* hu, const double* hw,
+              const double* time, double g, double* t_h, double* t_hu, double* t_hw,
+              nh_status* status, void* stream);
+int nh_pm_criterion(const nh_member* members, const nh_pm_member* pm, int m, int n_members,
+                    int n_elements, const double* h, const double* hu, const double* hw,
+                    const double* time, int kind, double* values, void* stream);
 
 /* Semi-discrete tendency, hydrostatic.rhs_operator (hydrostatic.py:88-184).
  * Outputs t_h, t_hu, t_hw [B][N][2]. */

@@ -51,28 +51,51 @@ def ptr(x) -> int | None:
 BC_CODE = {"absorbing": _lib.BC_ABSORBING, "wall": _lib.BC_WALL}
 
 
-def member_record(grid, bathy, bcs, dt: float | None) -> np.ndarray:
-    """One nh_member record (include/nhswe_b200.h) for a (grid, bottom, bcs, dt)."""
-    if grid.poly_order != 1:
-        raise NotImplementedError("the B200 kernels implement the P1 discretisation only")
+def member_record(grid, bathy, bcs, dt: float | None, any_order: bool = False) -> np.ndarray:
+    """One nh_member record (include/nhswe_b200.h) for a (grid, bottom, bcs, dt).
+
+    The P1 kernels take their operators from it; for the m-node kernels
+    (any_order=True, orders p > 1) its P1 operator arrays stay zero and the
+    operators travel in pm_record(grid)."""
+    if grid.poly_order != 1 and not any_order:
+        raise NotImplementedError("this entry point implements the P1 discretisation only "
+                                  "(orders p > 1: heun_step, adaptive_step, simulate, "
+                                  "Ensemble, rhs_operator, criterion_values)")
     r = np.zeros(1, dtype=_lib.MEMBER_DTYPE)
     r["x_left"] = grid.x_left
     r["dx"] = grid.dx
     r["dt"] = 0.0 if dt is None else dt
     r["eps"] = 1e-9 * grid.dx
     r["two_over_dx"] = 2.0 / grid.dx
-    r["weak_div"] = grid.weak_div.ravel()
-    r["lift_left"] = grid.lift_left
-    r["lift_right"] = grid.lift_right
-    r["mass"] = grid.mass.ravel()
-    r["stiffness"] = grid.stiffness.ravel()
-    r["deriv_ref"] = grid.deriv_ref.ravel()
+    if grid.poly_order == 1:
+        r["weak_div"] = grid.weak_div.ravel()
+        r["lift_left"] = grid.lift_left
+        r["lift_right"] = grid.lift_right
+        r["mass"] = grid.mass.ravel()
+        r["stiffness"] = grid.stiffness.ravel()
+        r["deriv_ref"] = grid.deriv_ref.ravel()
     kind, params = bathy.pack()
     r["bottom_kind"] = kind
     r["bottom"][0, :len(params)] = params
     if bcs is not None:
         r["bc_left"] = BC_CODE[bcs.left.kind]
         r["bc_right"] = BC_CODE[bcs.right.kind]
+    return r
+
+
+def pm_record(grid) -> np.ndarray:
+    """One nh_pm_member record: the grid's m-node operators (the reference
+    GridSpec values, grid.py:79-114) and node offsets 0.5*dx*(ref + 1)."""
+    m = grid.poly_order + 1
+    if m > _lib.PM_MAX_NODES:
+        raise NotImplementedError(f"poly_order {grid.poly_order}: the kernels take m <= "
+                                  f"{_lib.PM_MAX_NODES} nodes per element")
+    r = np.zeros(1, dtype=_lib.PM_DTYPE)
+    for f in ("weak_div", "mass", "stiffness", "deriv_ref"):
+        r[f][0, :m * m] = np.ascontiguousarray(getattr(grid, f)).ravel()
+    r["lift_left"][0, :m] = grid.lift_left
+    r["lift_right"][0, :m] = grid.lift_right
+    r["node_off"][0, :m] = 0.5 * grid.dx * (grid.ref_nodes + 1.0)
     return r
 
 
@@ -191,6 +214,31 @@ def advance(members, h, hu, hw, time, n_steps, sch, status, flag_bits=None, p_ou
     rc = lib.nh_advance(ptr(members), B, N, ptr(h), ptr(hu), ptr(hw), ptr(time), int(n_steps),
                         ctypes.byref(sch), ctypes.byref(out), ptr(status), stream_ptr())
     _lib.check(rc, "nh_advance")
+
+
+_pm_ws = {}
+
+
+def pm_workspace(m: int, B: int, N: int):
+    n = int(require_cuda().nh_pm_workspace_bytes(m, B, N))
+    ws = _pm_ws.get("ws")
+    if ws is None or ws.numel() < n:
+        ws = torch().empty(n, dtype=torch().uint8, device="cuda")
+        _pm_ws["ws"] = ws
+    return ws
+
+
+def pm_advance(members, pm, h, hu, hw, time, n_steps, sch, status, flag_bits=None, p_out=None,
+               gauges=None):
+    """Enqueue nh_pm_advance (m-node kernels; h, hu, hw CUDA [B][N][m]) in place."""
+    lib = require_cuda()
+    B, N, m = h.shape[0], h.shape[1], h.shape[2]
+    out = _outputs(flag_bits, p_out, None, gauges)
+    ws = pm_workspace(m, B, N)
+    rc = lib.nh_pm_advance(ptr(members), ptr(pm), m, B, N, ptr(h), ptr(hu), ptr(hw), ptr(time),
+                           int(n_steps), ctypes.byref(sch), ctypes.byref(out), ptr(status),
+                           ptr(ws), ws.numel(), stream_ptr())
+    _lib.check(rc, "nh_pm_advance")
 
 
 def stream_workspace(B: int, N: int):

@@ -35,7 +35,13 @@ MEMBER_DTYPE = np.dtype([
 ])
 STATUS_DTYPE = np.dtype([("error_key", "u8"), ("cfl_max", "f8"), ("flagged", "i8"),
                          ("steps_done", "i4"), ("any_hw", "i4")])
-assert MEMBER_DTYPE.itemsize == 312 and STATUS_DTYPE.itemsize == 32
+PM_DTYPE = np.dtype([   # nh_pm_member: m-node operators, m <= 4 (row-major, leading dim m)
+    ("weak_div", "f8", (16,)), ("lift_left", "f8", (4,)), ("lift_right", "f8", (4,)),
+    ("mass", "f8", (16,)), ("stiffness", "f8", (16,)), ("deriv_ref", "f8", (16,)),
+    ("node_off", "f8", (4,)),
+])
+PM_MAX_NODES = 4
+assert MEMBER_DTYPE.itemsize == 312 and STATUS_DTYPE.itemsize == 32 and PM_DTYPE.itemsize == 608
 
 
 class Scheme(ctypes.Structure):
@@ -51,14 +57,15 @@ class Outputs(ctypes.Structure):
                 ("gauge_h", ctypes.c_void_p), ("n_gauges", ctypes.c_int32)]
 
 
-ABI_VERSION = 2   # include/nhswe_b200.h NH_ABI_VERSION
+ABI_VERSION = 3   # include/nhswe_b200.h NH_ABI_VERSION
 
 EXPORTS = ("nh_abi_version", "nh_advance", "nh_stream_advance", "nh_stream_workspace_bytes",
            "nh_rhs", "nh_criterion", "nh_coefficients",
            "nh_ldg_solve", "nh_correct_momentum", "nh_bottom_sample", "nh_plan",
            "nh_last_cuda_error", "nh_stream_graphs", "nh_stream_timing", "nh_stream_kernel_times",
            "nh_launch_count",
-           "nh_selftest_arith")
+           "nh_selftest_arith", "nh_pm_workspace_bytes", "nh_pm_advance", "nh_pm_rhs",
+           "nh_pm_criterion")
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -84,6 +91,11 @@ _SIGS = {
     "nh_plan": ([_I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I),
                  ctypes.POINTER(_I)], _I),
     "nh_last_cuda_error": ([], ctypes.c_char_p),
+    "nh_pm_workspace_bytes": ([_I, _I, _I], ctypes.c_size_t),
+    "nh_pm_advance": ([_P, _P, _I, _I, _I, _P, _P, _P, _P, _I, ctypes.POINTER(Scheme),
+                       ctypes.POINTER(Outputs), _P, _P, ctypes.c_size_t, _P], _I),
+    "nh_pm_rhs": ([_P, _P, _I, _I, _I, _P, _P, _P, _P, _D, _P, _P, _P, _P, _P], _I),
+    "nh_pm_criterion": ([_P, _P, _I, _I, _I, _P, _P, _P, _P, _I, _P, _P], _I),
 }
 
 _lib = None

@@ -80,13 +80,20 @@ def enlarge_flags(flags: np.ndarray) -> np.ndarray:
 def _criterion_device(predictor: FlowState, bathy: BathymetryModel, kind: str):
     lib = D.require_cuda()
     grid = predictor.grid
-    m = D.upload_members(D.member_record(grid, bathy, None, None))
+    pm = grid.poly_order != 1
+    m = D.upload_members(D.member_record(grid, bathy, None, None, any_order=pm))
     h, hu, hw = _upload_state(predictor)
     t = D.dev(np.array([predictor.time]))
     out = D.torch().empty_like(h)
-    _lib.check(lib.nh_criterion(D.ptr(m), 1, grid.n_elements, D.ptr(h), D.ptr(hu), D.ptr(hw),
-                                D.ptr(t), _lib.CRIT[kind], D.ptr(out), D.stream_ptr()),
-               "nh_criterion")
+    if pm:
+        _lib.check(lib.nh_pm_criterion(D.ptr(m), D.ptr(D.upload_members(D.pm_record(grid))),
+                                       grid.poly_order + 1, 1, grid.n_elements, D.ptr(h),
+                                       D.ptr(hu), D.ptr(hw), D.ptr(t), _lib.CRIT[kind],
+                                       D.ptr(out), D.stream_ptr()), "nh_pm_criterion")
+    else:
+        _lib.check(lib.nh_criterion(D.ptr(m), 1, grid.n_elements, D.ptr(h), D.ptr(hu),
+                                    D.ptr(hw), D.ptr(t), _lib.CRIT[kind], D.ptr(out),
+                                    D.stream_ptr()), "nh_criterion")
     return out[0]
 
 

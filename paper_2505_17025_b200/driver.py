@@ -65,20 +65,27 @@ class Ensemble:
     CUDA float64 tensors (B, N, 2); time: CUDA float64 (B,).
     """
 
-    def __init__(self, records: np.ndarray, h, hu, hw, time=None):
+    def __init__(self, records: np.ndarray, h, hu, hw, time=None, pm_records=None):
         T = D.torch()
         D.require_cuda()
         self.records = np.ascontiguousarray(records)
         self.members = D.upload_members(self.records)
         self.B, self.N = int(h.shape[0]), int(h.shape[1])
+        self.M = int(h.shape[2])   # nodes per element (poly_order + 1)
+        # m-node operators (D.pm_record per member): required for M != 2, and
+        # selects the generic m-node kernels for M == 2 with path="generic"
+        self.pm = None if pm_records is None else D.upload_members(
+            np.ascontiguousarray(pm_records))
+        if self.M != 2 and self.pm is None:
+            raise ValueError("orders p > 1 need the members' pm_records (D.pm_record)")
         self.h, self.hu, self.hw = h, hu, hw
         self.time = time if time is not None else T.zeros(self.B, dtype=T.float64, device="cuda")
         self.status = D.new_status(self.B)
 
     @classmethod
-    def from_host(cls, records, h, hu, hw, time=None):
+    def from_host(cls, records, h, hu, hw, time=None, pm_records=None):
         t = D.dev(np.zeros(len(records)) if time is None else np.asarray(time, dtype=np.float64))
-        return cls(records, D.dev(h), D.dev(hu), D.dev(hw), t)
+        return cls(records, D.dev(h), D.dev(hu), D.dev(hw), t, pm_records)
 
     def reset_status(self):
         self.status = D.new_status(self.B)
@@ -90,7 +97,10 @@ class Ensemble:
         and config 4 (0.83 vs 4.4 ms/step), tools/scenario_paths.py,
         tools/path_compare.py.  Every mode and criterion runs on it (the w /
         w_x first-step fallback of adaptivity.py:153 is K_F); the resident
-        kernel stays available as path="resident"."""
+        kernel stays available as path="resident".  Orders p > 1 run the
+        m-node kernels ("generic")."""
+        if self.M != 2:
+            return "generic"
         return "stream"
 
     def stream_chunk(self, budget: int | None = None) -> int:
@@ -123,6 +133,12 @@ class Ensemble:
         sch = D.scheme(_MODES[mode], c.kind, c.k_nh, c.enlarge, flux, g, rho)
         if path == "auto":
             path = self.choose_path(mode, criterion)
+        if self.M != 2 or path == "generic":   # m-node kernels (orders p > 1)
+            if self.pm is None:
+                raise ValueError("path='generic' needs pm_records")
+            D.pm_advance(self.members, self.pm, self.h, self.hu, self.hw, self.time, n_steps,
+                         sch, self.status, flag_bits, p_out, gauges)
+            return
         if path == "stream":
             chunk = self.stream_chunk()
             if getattr(self, "_ws", None) is None:
@@ -172,9 +188,12 @@ def simulate(spec: ScenarioSpec, initial: FlowState, mode: str,
     grid = spec.grid
     n = grid.n_elements
     n_steps = spec.n_steps
-    rec = D.member_record(grid, spec.bathymetry, spec.bcs, spec.dt)
+    pm = grid.poly_order != 1
+    rec = D.member_record(grid, spec.bathymetry, spec.bcs, spec.dt, any_order=pm)
     ens = Ensemble.from_host(rec, initial.h.values[None], initial.hu.values[None],
-                             initial.hw.values[None], [initial.time])
+                             initial.hw.values[None], [initial.time],
+                             D.pm_record(grid) if pm else None)
+    m_nodes = grid.poly_order + 1
     nw = (n + 31) // 32
     record = record_masks and mode == "adaptive"
     gauge_idx = [grid.nearest_node(x) for x in spec.gauges]
@@ -195,7 +214,8 @@ def simulate(spec: ScenarioSpec, initial: FlowState, mode: str,
         # device after every step (no per-step synchronisation)
         gauges = None
         if per_step:
-            nodes = T.as_tensor([2 * e + j for e, j in gauge_idx], dtype=T.int32, device="cuda")
+            nodes = T.as_tensor([m_nodes * e + j for e, j in gauge_idx], dtype=T.int32,
+                                device="cuda")
             gauges = (nodes, T.empty((n_steps, 1, len(gauge_idx)), dtype=T.float64,
                                      device="cuda"))
         ev0.record()

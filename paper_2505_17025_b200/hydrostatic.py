@@ -66,14 +66,21 @@ def rhs_operator(state: FlowState, bathy: BathymetryModel, bcs: BoundaryPair,
     """Semi-discrete tendency at the state's time (hydrostatic.py:88-184)."""
     lib = D.require_cuda()
     grid = state.grid
-    m = D.upload_members(D.member_record(grid, bathy, bcs, None))
+    pm = grid.poly_order != 1
+    m = D.upload_members(D.member_record(grid, bathy, bcs, None, any_order=pm))
     h, hu, hw = _upload_state(state)
     t = D.dev(np.array([state.time]))
     out = [D.torch().empty_like(h) for _ in range(3)]
     st = D.new_status(1)
-    _lib.check(lib.nh_rhs(D.ptr(m), 1, grid.n_elements, D.ptr(h), D.ptr(hu), D.ptr(hw), D.ptr(t),
-                          g, D.ptr(out[0]), D.ptr(out[1]), D.ptr(out[2]), D.ptr(st),
-                          D.stream_ptr()), "nh_rhs")
+    if pm:
+        _lib.check(lib.nh_pm_rhs(D.ptr(m), D.ptr(D.upload_members(D.pm_record(grid))),
+                                 grid.poly_order + 1, 1, grid.n_elements, D.ptr(h), D.ptr(hu),
+                                 D.ptr(hw), D.ptr(t), g, D.ptr(out[0]), D.ptr(out[1]),
+                                 D.ptr(out[2]), D.ptr(st), D.stream_ptr()), "nh_pm_rhs")
+    else:
+        _lib.check(lib.nh_rhs(D.ptr(m), 1, grid.n_elements, D.ptr(h), D.ptr(hu), D.ptr(hw),
+                              D.ptr(t), g, D.ptr(out[0]), D.ptr(out[1]), D.ptr(out[2]),
+                              D.ptr(st), D.stream_ptr()), "nh_rhs")
     status = D.read_status(st)
     err = D.decode_error(status["error_key"][0])
     if err is not None:
@@ -96,7 +103,10 @@ def _advance_one(state: FlowState, dt: float, bathy, bcs, mode: int, g: float, r
     """One fused step of a single member; returns host arrays + flags/p/status."""
     grid = state.grid
     T = D.torch()
-    m = D.upload_members(D.member_record(grid, bathy, bcs, dt))
+    pm = grid.poly_order != 1
+    if pm and given is not None:
+        raise NotImplementedError("apply_correction on given ranges: P1 only")
+    m = D.upload_members(D.member_record(grid, bathy, bcs, dt, any_order=pm))
     h, hu, hw = _upload_state(state)
     t = D.dev(np.array([state.time]))
     st = D.new_status(1)
@@ -105,7 +115,10 @@ def _advance_one(state: FlowState, dt: float, bathy, bcs, mode: int, g: float, r
     p = T.zeros_like(h) if want_p else None
     gv = D.dev(np.asarray(given, np.uint32).view(np.int32), dtype=np.int32) if given is not None else None
     sch = D.scheme(mode, kind, k_nh, enlarge, flux, g, rho)
-    D.advance(m, h, hu, hw, t, 1, sch, st, fb, p, gv)
+    if pm:   # orders p > 1: the m-node kernels (csrc/pm_kernels.cu)
+        D.pm_advance(m, D.upload_members(D.pm_record(grid)), h, hu, hw, t, 1, sch, st, fb, p)
+    else:
+        D.advance(m, h, hu, hw, t, 1, sch, st, fb, p, gv)
     status = D.read_status(st)
     out = dict(h=h[0].cpu().numpy(), hu=hu[0].cpu().numpy(), hw=hw[0].cpu().numpy(),
                time=float(t.item()), status=status)
