@@ -117,9 +117,45 @@ def grid_ops(out):
             out[f"grid_p{p}_{f}"] = np.asarray(getattr(g, f))
 
 
+SIMS = {   # full simulate() runs of the paper scenarios at p = 2, 3 (driver.py:50-103)
+    "sim_solitary_p2": dict(scenario="solitary", over=dict(poly_order=2, n_elements=120,
+                                                           dt=0.05, t_end=15.0),
+                            gauges=(150.0, 260.0), mode="adaptive", kind="eta_over_d",
+                            enlarge=True),
+    "sim_solitary_p3": dict(scenario="solitary", over=dict(poly_order=3, n_elements=100,
+                                                           dt=0.04, t_end=8.0),
+                            gauges=(200.0,), mode="global"),
+    "sim_hammack_p2": dict(scenario="hammack_up", over=dict(poly_order=2, dx=0.05, dt=0.004,
+                                                            t_end=2.0),
+                           gauges=(0.61, 1.61), mode="adaptive", kind="eta_over_d",
+                           enlarge=False),
+}
+
+
+def sim_case(name, c, out):
+    from dataclasses import replace
+
+    from nhswe.driver import simulate
+    from nhswe.scenarios import build_scenario
+    spec, init = build_scenario(c["scenario"], **c["over"])
+    spec = replace(spec, gauges=tuple(c["gauges"]))
+    crit = Criterion(c["kind"], 1e-3, c["enlarge"]) if c["mode"] == "adaptive" else None
+    r = simulate(spec, init, c["mode"], crit)
+    out[f"{name}_cfg"] = np.array(json.dumps(c))
+    out[f"{name}_h"], out[f"{name}_hu"], out[f"{name}_hw"] = (r.final_state.h.values,
+                                                             r.final_state.hu.values,
+                                                             r.final_state.hw.values)
+    out[f"{name}_gauge_eta"] = r.gauge_eta
+    out[f"{name}_gauge_t"] = r.gauge_times
+    out[f"{name}_frac"] = np.float64(r.mask_fraction_mean)
+    print(f"{name}: {spec.n_steps} steps, mask fraction {r.mask_fraction_mean:.4f}")
+
+
 def main():
-    out = {"cases": np.array(json.dumps(list(CASES)))}
+    out = {"cases": np.array(json.dumps(list(CASES))), "sims": np.array(json.dumps(list(SIMS)))}
     grid_ops(out)
+    for name, c in SIMS.items():
+        sim_case(name, c, out)
     for name, spec in CASES.items():
         run_case(name, spec, out)
     np.savez_compressed(os.path.join(HERE, "pm.npz"), **out)

@@ -117,3 +117,24 @@ def test_generic_kernels_at_p1_match_stream_path(mode, kind, enlarge):
         assert rel(gh[i] - h0, sh[i] - h0) <= 1e-9, i
         assert rel(gq[i], sq[i]) <= 1e-9, i
         assert np.abs(gw[i] - sw[i]).max() <= 1e-9 * max(np.abs(sw[i]).max(), 1e-12), i
+
+
+@pytest.mark.parametrize("name", json.loads(str(GOLD["sims"])))
+def test_simulate_paper_scenarios_high_order(name):
+    """simulate() of the paper scenarios at p = 2, 3 (gauges recorded on the
+    device at flat node index e*m + j) against the reference's simulate()."""
+    from dataclasses import replace
+    c = json.loads(str(GOLD[f"{name}_cfg"]))
+    spec, init = P.build_scenario(c["scenario"], **c["over"])
+    spec = replace(spec, gauges=tuple(c["gauges"]))
+    crit = P.Criterion(c["kind"], 1e-3, c["enlarge"]) if c["mode"] == "adaptive" else None
+    r = P.simulate(spec, init, c["mode"], crit)
+    d = spec.bathymetry.depth(spec.grid.sample_nodes, r.final_state.time)
+    e_eta = rel(r.final_state.h.values - d, GOLD[f"{name}_h"] - d)
+    e_hu = rel(r.final_state.hu.values, GOLD[f"{name}_hu"])
+    e_g = rel(r.gauge_eta, GOLD[f"{name}_gauge_eta"])
+    print(f"{name}: {spec.n_steps} steps, eta {e_eta:.1e} hu {e_hu:.1e} gauges {e_g:.1e}, "
+          f"mask fraction {r.mask_fraction_mean:.4f} (reference {float(GOLD[f'{name}_frac']):.4f})")
+    assert e_eta <= 1e-9 and e_hu <= 1e-9 and e_g <= 1e-9
+    assert np.array_equal(r.gauge_times, GOLD[f"{name}_gauge_t"])
+    assert abs(r.mask_fraction_mean - float(GOLD[f"{name}_frac"])) <= 1e-12
