@@ -141,8 +141,8 @@ int nh_advance(const nh_member* members, int n_members, int n_elements,
                nh_status* status, void* stream);
 
 /* Streaming variant of nh_advance for large ensembles (same contract and
- * in-place semantics; modes HYDROSTATIC / GLOBAL / ADAPTIVE with the
- * eta_over_d, eta_x, u, u_x criteria).  Every step is four kernels over
+ * in-place semantics; modes HYDROSTATIC / GLOBAL / ADAPTIVE, every criterion --
+ * the w / w_x all-zero-input fallback is one more kernel).  Every step is four kernels over
  * independent 120-element tiles of 128 threads (K_P predictor+criterion, K_S condensation,
  * K_X per-member tile chain, K_C reconstruction) with the vertical-momentum
  * update fused into the next step's load; state goes through HBM once per
