@@ -213,6 +213,14 @@ struct KpSmem {
 
 
 
+// (h p) traces of the pending correction: the sf planes (the warp-exchange
+// variant keeps them in its sh)
+#if NH_KP_WARP_XCHG
+#define NH_HP_TRACES(ks) ((ks).sh)
+#else
+#define NH_HP_TRACES(ks) ((ks).sf)
+#endif
+
 struct KsSmem {
   double wnode[NW * 31 * 6];
   double wagg[NW * 6];
@@ -358,9 +366,9 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
             RADD(q.w0, RMUL(dt, k1[4])), RADD(q.w1, RMUL(dt, k1[5]))};
   }
   bad |= (own && !(qs.h0 > 0.0 && qs.h1 > 0.0)) ? 2u : 0u;
-#if !NH_KP_WARP_XCHG
-  __syncthreads();   // every read of sh / sf of stage 1 is done
-#endif
+  // (no barrier before stage 2: its sh writes follow stage 1's sf barrier,
+  // which every stage-1 sh read precedes, and its sf writes follow its own
+  // sh barrier, which every stage-1 sf read precedes)
 
   // ---------------- Heun stage 2 at t + dt ----------------
   double k2[6], d0, d1;   // d0, d1: depth at t + dt, reused by the criterion
@@ -514,7 +522,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
 
 // The previous step's pending hw correction of the thread's element (q.w
 // updated in place) and the step body.  On entry the (h p) traces are in
-// ks.sh, made visible by the caller's barrier.
+// NH_HP_TRACES(ks), made visible by the caller's barrier.
 // hw += dt/rho (6/quad p + d_x/quad (h p)_x + phi) on flagged elements
 // (corrector.py:441-482); (h p)_x lifts use the neighbours' (h p) traces.
 template <class SM>
@@ -527,7 +535,7 @@ __device__ __forceinline__ void kp_correct_and_step(const StreamArgs& a, const T
   const double hp0 = q.h0 * p0, hp1 = q.h1 * p1;
   double bp0 = 0.0, bp1 = 0.0;
   if (f) {
-    const double* sh = ks.sh;
+    const double* sh = NH_HP_TRACES(ks);
     auto hp_of = [&](int ee, int node, int slot) -> double {
       if (slot >= 0 && slot < TPB) return sh[node * TPB + slot];
       // neighbour outside the CTA's slots (never needed for own elements)
@@ -552,7 +560,8 @@ __device__ __forceinline__ void kp_correct_and_step(const StreamArgs& a, const T
     bp0 = nh_div(6.0, qd0) * p0 + nh_div(dx0, qd0) * hx0 + phi0;
     bp1 = nh_div(6.0, qd1) * p1 + nh_div(dx1, qd1) * hx1 + phi1;
   }
-  __syncthreads();   // every read of the (h p) traces done before sh is reused
+  // (no barrier: the traces live in the sf planes, which stage 1 first
+  // writes after its sh barrier, i.e. after every thread's reads here)
   if (f) {
     q.w0 += mc.lk.cdt * bp0;
     q.w1 += mc.lk.cdt * bp1;
@@ -603,8 +612,8 @@ __device__ __forceinline__ void kp_tile(const StreamArgs& a, const TileIdx& ti, 
   }
   load_member(a, b, msh, mc);
   if (a.pend) {
-    ks.sh[0 * TPB + i] = q.h0 * p0;
-    ks.sh[1 * TPB + i] = q.h1 * p1;
+    NH_HP_TRACES(ks)[0 * TPB + i] = q.h0 * p0;
+    NH_HP_TRACES(ks)[1 * TPB + i] = q.h1 * p1;
   }
   __syncthreads();
   kp_correct_and_step(a, ti, msh, mc, ks, ks.sq, q, f, p0, p1, phi0, phi1, dx0, dx1);
@@ -693,8 +702,8 @@ __device__ __forceinline__ void kp_tile_staged(const StreamArgs& a, const TileId
     p0 = pv[0]; p1 = pv[BN]; phi0 = pv[2 * BN]; phi1 = pv[3 * BN]; dx0 = pv[4 * BN]; dx1 = pv[5 * BN];
   }
   if (a.pend) {
-    ks.sh[0 * TPB + i] = q.h0 * p0;
-    ks.sh[1 * TPB + i] = q.h1 * p1;
+    NH_HP_TRACES(ks)[0 * TPB + i] = q.h0 * p0;
+    NH_HP_TRACES(ks)[1 * TPB + i] = q.h1 * p1;
   }
   __syncthreads();
   kp_correct_and_step(a, ti, st.m, st.mc, ks, st.q, q, f, p0, p1, phi0, phi1, dx0, dx1);
