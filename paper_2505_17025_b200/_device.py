@@ -59,8 +59,8 @@ def member_record(grid, bathy, bcs, dt: float | None, any_order: bool = False) -
     operators travel in pm_record(grid)."""
     if grid.poly_order != 1 and not any_order:
         raise NotImplementedError("this entry point implements the P1 discretisation only "
-                                  "(orders p > 1: heun_step, adaptive_step, simulate, "
-                                  "Ensemble, rhs_operator, criterion_values)")
+                                  "(orders p > 1: heun_step, adaptive_step, apply_correction, "
+                                  "simulate, Ensemble, rhs_operator, criterion_values)")
     r = np.zeros(1, dtype=_lib.MEMBER_DTYPE)
     r["x_left"] = grid.x_left
     r["dx"] = grid.dx
@@ -229,11 +229,11 @@ def pm_workspace(m: int, B: int, N: int):
 
 
 def pm_advance(members, pm, h, hu, hw, time, n_steps, sch, status, flag_bits=None, p_out=None,
-               gauges=None):
+               gauges=None, given=None):
     """Enqueue nh_pm_advance (m-node kernels; h, hu, hw CUDA [B][N][m]) in place."""
     lib = require_cuda()
     B, N, m = h.shape[0], h.shape[1], h.shape[2]
-    out = _outputs(flag_bits, p_out, None, gauges)
+    out = _outputs(flag_bits, p_out, given, gauges)
     ws = pm_workspace(m, B, N)
     rc = lib.nh_pm_advance(ptr(members), ptr(pm), m, B, N, ptr(h), ptr(hu), ptr(hw), ptr(time),
                            int(n_steps), ctypes.byref(sch), ctypes.byref(out), ptr(status),

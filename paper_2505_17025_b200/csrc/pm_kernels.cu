@@ -63,6 +63,7 @@ struct PmArgs {
   const int32_t* gauge_nodes;
   double* gauge_h;
   int n_gauges;
+  const uint32_t* given;   // NH_MODE_CORRECT_GIVEN: [B][ceil(N/32)] ranges to correct
   int step;
   int corr;         // the step has a correction (mode != hydrostatic)
   nh_scheme sch;
@@ -306,7 +307,9 @@ __global__ void __launch_bounds__(PTB) pm_flags(PmArgs a) {
   const int N = a.N, b = idx / N, e = idx - b * N;
   bool f = true;   // global mode, and the w / w_x fallback (adaptivity.py:153-154)
   const bool wcrit = a.sch.criterion == NH_CRIT_W || a.sch.criterion == NH_CRIT_W_X;
-  if (a.sch.mode == NH_MODE_ADAPTIVE && !(wcrit && !a.hw_any[b])) {
+  if (a.given) {   // apply_correction on given ranges (corrector.py:485-498)
+    f = (a.given[(size_t)b * ((N + 31) / 32) + (e >> 5)] >> (e & 31)) & 1u;
+  } else if (a.sch.mode == NH_MODE_ADAPTIVE && !(wcrit && !a.hw_any[b])) {
     f = a.raw[idx] != 0;
     if (a.sch.enlarge) {   // enlarge_flags (adaptivity.py:99-104)
       if (e > 0) f = f || a.raw[idx - 1];
@@ -375,7 +378,9 @@ __global__ void __launch_bounds__(PTB) pm_condense(PmArgs a) {
   const nh_pm_member& c = a.pm[b];
   const nh_scheme& sch = a.sch;
   const Elem<M> q = load_elem<M>(a.h_out, a.hu_out, a.hw_out, o);
-  const BottomTime bt1 = bottom_time(m, a.time[b] + m.dt);
+  // coefficients at the predictor's time: t + dt in a step, the given state's
+  // own time for apply_correction
+  const BottomTime bt1 = bottom_time(m, a.given ? a.time[b] : a.time[b] + m.dt);
   const LdgConst lk = make_ldg_const(m.dt, sch.g, sch.rho);
   Chan ch[M];
   double eta[M], hx[M], ex[M];
@@ -477,6 +482,7 @@ __global__ void __launch_bounds__(PTB) pm_chain(PmArgs a) {
       a.io[k] = fma(a.chain[BN + k], z, a.chain[k]);
     }
   }
+  if (a.given) return;             // apply_correction: the time stays
   a.time[b] = a.time[b] + m.dt;   // t + dt per step (hydrostatic.py:206-209)
   a.status[b].steps_done += 1;
   if (a.hw_any) a.hw_any[b] = 0;
@@ -621,6 +627,20 @@ int pm_advance_m(PmArgs a, int n_steps, double** A, double** Bb, const nh_output
                  cudaStream_t s) {
   const int BN = a.B * a.N;
   void* args[1] = {&a};
+  if (a.given) {   // the correction alone, in place on the given predictor state
+    a.h_in = a.h_out = A[0]; a.hu_in = a.hu_out = A[1]; a.hw_in = a.hw_out = A[2];
+    a.step = 0;
+    int rc = launch((void*)pm_flags, BN, args, s);
+    if (!rc) rc = launch((void*)pm_condense<M>, BN, args, s);
+    if (!rc) rc = launch((void*)pm_chain<M>, a.B, args, s);
+    if (!rc) rc = launch((void*)pm_reconstruct<M>, BN, args, s);
+    if (!rc) rc = launch((void*)pm_correct<M>, BN, args, s);
+    if (!rc && out && out->p_nh &&
+        cudaMemcpyAsync(out->p_nh, a.p, (size_t)BN * M * 8, cudaMemcpyDeviceToDevice, s) !=
+            cudaSuccess)
+      rc = NH_E_CUDA;
+    return rc;
+  }
   for (int k = 0; k < n_steps; ++k) {
     double** in = (k & 1) ? Bb : A;
     double** ou = (k & 1) ? A : Bb;
@@ -669,7 +689,9 @@ int nh_pm_advance(const nh_member* members, const nh_pm_member* pm, int m, int B
   if ((long long)B * N >= (1ll << 31)) return NH_E_UNSUPPORTED;
   if (workspace_bytes < nh_pm_workspace_bytes(m, B, N)) return NH_E_ARG;
   const nh_scheme& sc = *scheme;
-  if (sc.mode < NH_MODE_HYDROSTATIC || sc.mode > NH_MODE_ADAPTIVE) return NH_E_UNSUPPORTED;
+  if (sc.mode < NH_MODE_HYDROSTATIC || sc.mode > NH_MODE_CORRECT_GIVEN) return NH_E_UNSUPPORTED;
+  if (sc.mode == NH_MODE_CORRECT_GIVEN && (!outputs || !outputs->given_flags || n_steps != 1))
+    return NH_E_ARG;
   if (sc.mode != NH_MODE_HYDROSTATIC && (sc.c12 != -0.5 || sc.c22 != 0.0)) return NH_E_UNSUPPORTED;
   if (n_steps == 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
@@ -703,6 +725,7 @@ int nh_pm_advance(const nh_member* members, const nh_pm_member* pm, int m, int B
     a.n_gauges = outputs->n_gauges;
   }
   a.corr = sc.mode != NH_MODE_HYDROSTATIC;
+  a.given = sc.mode == NH_MODE_CORRECT_GIVEN ? outputs->given_flags : nullptr;
   a.sch = sc; a.B = B; a.N = N;
   double* A[3] = {h, hu, hw};
   double* Bb[3] = {alt, alt + BNM, alt + 2 * BNM};

@@ -104,8 +104,6 @@ def _advance_one(state: FlowState, dt: float, bathy, bcs, mode: int, g: float, r
     grid = state.grid
     T = D.torch()
     pm = grid.poly_order != 1
-    if pm and given is not None:
-        raise NotImplementedError("apply_correction on given ranges: P1 only")
     m = D.upload_members(D.member_record(grid, bathy, bcs, dt, any_order=pm))
     h, hu, hw = _upload_state(state)
     t = D.dev(np.array([state.time]))
@@ -116,7 +114,8 @@ def _advance_one(state: FlowState, dt: float, bathy, bcs, mode: int, g: float, r
     gv = D.dev(np.asarray(given, np.uint32).view(np.int32), dtype=np.int32) if given is not None else None
     sch = D.scheme(mode, kind, k_nh, enlarge, flux, g, rho)
     if pm:   # orders p > 1: the m-node kernels (csrc/pm_kernels.cu)
-        D.pm_advance(m, D.upload_members(D.pm_record(grid)), h, hu, hw, t, 1, sch, st, fb, p)
+        D.pm_advance(m, D.upload_members(D.pm_record(grid)), h, hu, hw, t, 1, sch, st, fb, p,
+                     given=gv)
     else:
         D.advance(m, h, hu, hw, t, 1, sch, st, fb, p, gv)
     status = D.read_status(st)

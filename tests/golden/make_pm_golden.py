@@ -79,6 +79,9 @@ CASES = {
 }
 
 
+CORR = {"p2_flat_adaptive": [(3, 14), (20, 31)], "p3_plate_global": [(0, 9), (15, 39)]}
+
+
 def run_case(name, spec, out):
     grid = GridSpec(spec["xl"], spec["xr"], spec["n"], spec["p"])
     bathy = bottom_of(spec)
@@ -104,6 +107,12 @@ def run_case(name, spec, out):
     out[f"{name}_t"] = np.float64(st.time)
     out[f"{name}_p"] = p.values if p is not None else np.zeros_like(h)
     out[f"{name}_counts"] = np.array(counts)
+    if name in CORR:   # apply_correction on given ranges, the final state as predictor
+        from nhswe.corrector import apply_correction
+        cst, sol = apply_correction(st, bathy, spec["dt"], CORR[name], bcs)
+        out[f"{name}_corr_ranges"] = np.array(CORR[name])
+        out[f"{name}_corr_hu"], out[f"{name}_corr_hw"] = cst.hu.values, cst.hw.values
+        out[f"{name}_corr_p"] = sol.p_nh.values
     print(f"{name}: {spec['steps']} steps, flagged per step {counts[:3]}...{counts[-3:]}, "
           f"|hw| {np.abs(st.hw.values).max():.3e}")
 

@@ -138,3 +138,19 @@ def test_simulate_paper_scenarios_high_order(name):
     assert e_eta <= 1e-9 and e_hu <= 1e-9 and e_g <= 1e-9
     assert np.array_equal(r.gauge_times, GOLD[f"{name}_gauge_t"])
     assert abs(r.mask_fraction_mean - float(GOLD[f"{name}_frac"])) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["p2_flat_adaptive", "p3_plate_global"])
+def test_apply_correction_given_ranges_high_order(name):
+    """apply_correction (corrector.py:485-498) on given ranges at p = 2, 3, the
+    final state of the reference run as the predictor."""
+    s, grid, bathy, bcs, _, _ = setup(name)
+    t = float(GOLD[f"{name}_t"])
+    pred = P.FlowState(P.NodalField(grid, GOLD[f"{name}_h"]), P.NodalField(grid, GOLD[f"{name}_hu"]),
+                       P.NodalField(grid, GOLD[f"{name}_hw"]), t)
+    ranges = [tuple(r) for r in GOLD[f"{name}_corr_ranges"].tolist()]
+    st, sol = P.apply_correction(pred, bathy, s["dt"], ranges, bcs)
+    assert st.h is pred.h and st.time == t
+    assert rel(st.hu.values, GOLD[f"{name}_corr_hu"]) <= 1e-10
+    assert rel(st.hw.values, GOLD[f"{name}_corr_hw"]) <= 1e-10
+    assert rel(sol.p_nh.values, GOLD[f"{name}_corr_p"]) <= 1e-10
