@@ -385,7 +385,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
                       (sc.criterion == NH_CRIT_W || sc.criterion == NH_CRIT_W_X);
   if (w_crit && !nh_stream_kp_records_hw_any()) return NH_E_UNSUPPORTED;
   if (w_crit && cudaMemsetAsync(hw_any, 0, 4 * (size_t)B, s) != cudaSuccess) return NH_E_CUDA;
-  static int ks_grid = 0, kc_grid = 0, kp_pf_grid = 0;   // persistent grids: resident CTAs x SMs
+  static int ks_grid = 0, kc_grid = 0;   // persistent grids: resident CTAs x SMs
   if (!ks_grid) {
     int dev = 0, sms = 0, nks = 0, nkc = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -398,18 +398,8 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
       return NH_E_CUDA;
     ks_grid = std::max(1, nks) * sms;
     kc_grid = std::max(1, nkc) * sms;
-    if (void* pf = nh_stream_kp_pf_ptr()) {   // persistent K_P: resident CTAs x SMs
-      int npf = 0;
-      if (cudaFuncSetAttribute(pf, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)nh_stream_kp_pf_smem()) != cudaSuccess ||
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&npf, pf, NH_STREAM_THREADS,
-                                                        nh_stream_kp_pf_smem()) != cudaSuccess)
-        return NH_E_CUDA;
-      kp_pf_grid = std::max(1, npf) * sms;
-    }
     if (getenv("NH_STREAM_VERBOSE"))
-      fprintf(stderr, "nh_stream: K_S grid %d, K_C grid %d, K_P persistent grid %d (smem %zu B)\n",
-              ks_grid, kc_grid, kp_pf_grid, nh_stream_kp_pf_smem());
+      fprintf(stderr, "nh_stream: K_S grid %d, K_C grid %d\n", ks_grid, kc_grid);
     if (const char* v = getenv("NH_KS_WAVES")) {   // diagnostics: grid = waves x resident CTAs
       int wv = atoi(v);
       if (wv > 0) { ks_grid *= wv; kc_grid *= wv; }
@@ -437,11 +427,6 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   const dim3 gs((unsigned)std::min<size_t>(ks_grid, BT)), gc((unsigned)std::min<size_t>(kc_grid, BT));
   void* kp = nh_stream_kernel(0);
   const size_t kp_smem = nh_stream_kp_smem();
-  // the steps' K_P: the persistent prefetching kernel unless disabled (NH_KP_PF=0)
-  static const bool use_pf = !getenv("NH_KP_PF") || atoi(getenv("NH_KP_PF")) != 0;
-  void* kp_step = (use_pf && kp_pf_grid) ? nh_stream_kp_pf_ptr() : kp;
-  const dim3 gps = kp_step == kp ? gp : dim3((unsigned)std::min<size_t>(kp_pf_grid, BT));
-  const size_t kps_smem = kp_step == kp ? kp_smem : nh_stream_kp_pf_smem();
   void* kx = nh_stream_kernel(1);
   void* kc = nh_stream_kernel(2);
   void* ks = nh_stream_kernel(3);
@@ -472,7 +457,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   auto launch_step = [&](int k, cudaStream_t st) -> int {
     set_step(k);
     void* args[1] = {&a};
-    int rc = stream_launch(kp_step, 0, gps, bpp, args, st, kps_smem);
+    int rc = stream_launch(kp, 0, gp, bpp, args, st, kp_smem);
     if (!rc && a.n_gauges > 0)
       rc = stream_launch(nh_stream_kernel(6), 5, dim3((unsigned)(((size_t)B * a.n_gauges + 127) / 128)),
                          dim3(128), args, st);

@@ -618,93 +618,3 @@ __device__ __forceinline__ void kp_tile(const StreamArgs& a, const TileIdx& ti, 
   __syncthreads();
   kp_correct_and_step(a, ti, msh, mc, ks, ks.sq, q, f, p0, p1, phi0, phi1, dx0, dx1);
 }
-
-// ------------------------------------------------- K_P, persistent + prefetch
-// A persistent grid (resident CTAs x SMs) strides over the (member, tile)
-// list; while a CTA computes tile L it has the state and member record of
-// its next tile L + G in flight into the other shared-memory stage
-// (cp.async), the next tile's pending flags and the member index of the tile
-// after that in registers.  The stage of the tile being computed doubles as
-// its step-start copy (sq), so the two stages cost one state plane set more
-// than KpSmem.
-struct __align__(16) KpStage {
-  double q[6 * TPB];   // [3][TPB] double2: (h0, h1), (hu0, hu1), (hw0, hw1)
-  nh_member m;
-  MemberConst mc;
-};
-struct __align__(16) KpSmemP {
-  double sh[5 * TPB];
-  double sf[3 * TPB];
-  double sk[6 * TPB];
-  unsigned long long wcfl[NW];
-  uint8_t rf[TPB];
-  KpStage st[2];
-};
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
-// issue the copies of tile (b, tile) into stage st (every thread its element;
-// threads 0..54 one word of the member record / step constants each)
-__device__ __forceinline__ void kp_prefetch(const StreamArgs& a, int b, int tile, KpStage& st) {
-  constexpr int MW = (int)(sizeof(nh_member) / 8);
-  const int i = threadIdx.x;
-  const int e = tile * OWN - H + i;
-  if (e >= 0 && e < a.N) {
-    const size_t o = ((size_t)b * a.N + e) * 2;
-    cp_async16(&st.q[0 * TPB + 2 * i], a.h_in + o);
-    cp_async16(&st.q[2 * TPB + 2 * i], a.hu_in + o);
-    cp_async16(&st.q[4 * TPB + 2 * i], a.hw_in + o);
-  } else {   // outside the domain: the defaults of kp_tile
-    double2* s2 = reinterpret_cast<double2*>(st.q);
-    s2[0 * TPB + i] = double2{1.0, 1.0};
-    s2[1 * TPB + i] = double2{0.0, 0.0};
-    s2[2 * TPB + i] = double2{0.0, 0.0};
-  }
-  if (i < MW)
-    cp_async8(reinterpret_cast<unsigned long long*>(&st.m) + i,
-              reinterpret_cast<const unsigned long long*>(a.members + b) + i);
-  else if (i < MW + 16)
-    cp_async8(reinterpret_cast<unsigned long long*>(&st.mc) + (i - MW),
-              reinterpret_cast<const unsigned long long*>(a.mconst + (size_t)b * 16) + (i - MW));
-  cp_async_commit();
-}
-
-// the raw pending-flag byte of the thread's element of tile (b, tile), loaded
-// from a clamped address so the load can stay in flight until the next tile
-// (validity and a.pend are applied where it is consumed)
-__device__ __forceinline__ uint8_t kp_pending_flag(const StreamArgs& a, int b, int tile) {
-  const int e = tile * OWN - H + (int)threadIdx.x;
-  const int ec = min(max(e, 0), a.N - 1);
-  return a.flags_prev[(size_t)b * a.N + ec];
-}
-
-// tile L of the stage st (its copies complete and visible), f = its pending flag
-__device__ __forceinline__ void kp_tile_staged(const StreamArgs& a, const TileIdx& ti,
-                                               KpStage& st, KpSmemP& ks, uint8_t fraw) {
-  const bool f = a.pend && ti.valid && fraw;
-  const int N = a.N, i = ti.i, b = ti.b, e = ti.e;
-  const double2* s2 = reinterpret_cast<const double2*>(st.q);
-  const double2 vh = s2[0 * TPB + i], vq = s2[1 * TPB + i], vw = s2[2 * TPB + i];
-  Q6 q{vh.x, vh.y, vq.x, vq.y, vw.x, vw.y};
-  double p0 = 0.0, p1 = 0.0, phi0 = 0.0, phi1 = 0.0, dx0 = 0.0, dx1 = 0.0;
-  if (f) {
-    const size_t BN = (size_t)a.B * N;
-    const double* pv = a.pend + (size_t)b * N + e;
-    p0 = pv[0]; p1 = pv[BN]; phi0 = pv[2 * BN]; phi1 = pv[3 * BN]; dx0 = pv[4 * BN]; dx1 = pv[5 * BN];
-  }
-  if (a.pend) {
-    NH_HP_TRACES(ks)[0 * TPB + i] = q.h0 * p0;
-    NH_HP_TRACES(ks)[1 * TPB + i] = q.h1 * p1;
-  }
-  __syncthreads();
-  kp_correct_and_step(a, ti, st.m, st.mc, ks, st.q, q, f, p0, p1, phi0, phi1, dx0, dx1);
-}
