@@ -230,6 +230,29 @@ int nh_pm_criterion(const nh_member* members, const nh_pm_member* pm, int m, int
                     int n_elements, const double* h, const double* hu, const double* hw,
                     const double* time, int kind, double* values, void* stream);
 
+/* Coefficient-level corrector functions for m nodes per element (fields
+ * [B][N][m]; coef = [7][B][N][m] planes s11, s12, s22, f1, f2, phi, d_x):
+ *  nh_pm_coefficients     phi_term + assemble_coefficients (corrector.py:100-170)
+ *                         at the state's time, dt from the member record;
+ *  nh_pm_ldg_solve        ldg_solve / solve_on_ranges (corrector.py:292-424) on
+ *                         the flagged ranges (flags [B][ceil(N/32)]),
+ *                         outer_right [B][N] = hu right of each element;
+ *                         writes p (0 off the ranges) and hu on the ranges;
+ *  nh_pm_correct_momentum correct_momentum (corrector.py:427-482): hw_out =
+ *                         hw + dt/rho * bottom pressure on the flagged elements. */
+int nh_pm_coefficients(const nh_member* members, const nh_pm_member* pm, int m, int n_members,
+                       int n_elements, const double* h, const double* hu, const double* hw,
+                       const double* time, double g, double rho, double* coef, void* stream);
+int nh_pm_ldg_solve(const nh_member* members, const nh_pm_member* pm, int m, int n_members,
+                    int n_elements, const double* coef, const uint32_t* flags,
+                    const double* outer_right, double rho, double c11, double c12, double c22,
+                    double* p, double* hu, nh_status* status, void* workspace,
+                    size_t workspace_bytes, void* stream);
+int nh_pm_correct_momentum(const nh_member* members, const nh_pm_member* pm, int m,
+                           int n_members, int n_elements, const double* h, const double* p,
+                           const double* coef, const uint32_t* flags, double rho,
+                           const double* hw, double* hw_out, void* stream);
+
 /* Semi-discrete tendency, hydrostatic.rhs_operator (hydrostatic.py:88-184).
  * Outputs t_h, t_hu, t_hw [B][N][2]. */
 int nh_rhs(const nh_member* members, int n_members, int n_elements,

@@ -65,7 +65,7 @@ EXPORTS = ("nh_abi_version", "nh_advance", "nh_stream_advance", "nh_stream_works
            "nh_last_cuda_error", "nh_stream_graphs", "nh_stream_timing", "nh_stream_kernel_times",
            "nh_launch_count",
            "nh_selftest_arith", "nh_pm_workspace_bytes", "nh_pm_advance", "nh_pm_rhs",
-           "nh_pm_criterion")
+           "nh_pm_criterion", "nh_pm_coefficients", "nh_pm_ldg_solve", "nh_pm_correct_momentum")
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -96,6 +96,10 @@ _SIGS = {
                        ctypes.POINTER(Outputs), _P, _P, ctypes.c_size_t, _P], _I),
     "nh_pm_rhs": ([_P, _P, _I, _I, _I, _P, _P, _P, _P, _D, _P, _P, _P, _P, _P], _I),
     "nh_pm_criterion": ([_P, _P, _I, _I, _I, _P, _P, _P, _P, _I, _P, _P], _I),
+    "nh_pm_coefficients": ([_P, _P, _I, _I, _I, _P, _P, _P, _P, _D, _D, _P, _P], _I),
+    "nh_pm_ldg_solve": ([_P, _P, _I, _I, _I, _P, _P, _P, _D, _D, _D, _D, _P, _P, _P, _P,
+                         ctypes.c_size_t, _P], _I),
+    "nh_pm_correct_momentum": ([_P, _P, _I, _I, _I, _P, _P, _P, _P, _D, _P, _P, _P], _I),
 }
 
 _lib = None

@@ -78,13 +78,21 @@ def _coef_planes(predictor: FlowState, bathy, dt, g, rho):
     """Device [7][1][N][2] planes s11, s12, s22, f1, f2, phi, d_x."""
     lib = D.require_cuda()
     grid = predictor.grid
-    m = D.upload_members(D.member_record(grid, bathy, None, dt))
+    nodes = grid.poly_order + 1
+    m = D.upload_members(D.member_record(grid, bathy, None, dt, any_order=nodes != 2))
     h, hu, hw = _upload_state(predictor)
     t = D.dev(np.array([predictor.time]))
-    coef = D.torch().empty((7, 1, grid.n_elements, 2), dtype=D.torch().float64, device="cuda")
-    _lib.check(lib.nh_coefficients(D.ptr(m), 1, grid.n_elements, D.ptr(h), D.ptr(hu), D.ptr(hw),
-                                   D.ptr(t), g, rho, D.ptr(coef), D.stream_ptr()),
-               "nh_coefficients")
+    coef = D.torch().empty((7, 1, grid.n_elements, nodes), dtype=D.torch().float64,
+                           device="cuda")
+    if nodes != 2:   # orders p > 1: the m-node kernels
+        _lib.check(lib.nh_pm_coefficients(D.ptr(m), D.ptr(D.upload_members(D.pm_record(grid))),
+                                          nodes, 1, grid.n_elements, D.ptr(h), D.ptr(hu),
+                                          D.ptr(hw), D.ptr(t), g, rho, D.ptr(coef),
+                                          D.stream_ptr()), "nh_pm_coefficients")
+    else:
+        _lib.check(lib.nh_coefficients(D.ptr(m), 1, grid.n_elements, D.ptr(h), D.ptr(hu),
+                                       D.ptr(hw), D.ptr(t), g, rho, D.ptr(coef),
+                                       D.stream_ptr()), "nh_coefficients")
     return coef.cpu().numpy()[:, 0]
 
 
@@ -131,24 +139,37 @@ def _solve_device(coeffs: EllipticCoefficients, ranges, outer_right: np.ndarray,
             raise ValueError(f"invalid element range {(e0, e1)}")
         if e0 - off < 0 or e1 - off >= len(coeffs.s11):
             raise ValueError(f"range {(e0, e1)} outside the coefficient window")
-    planes = np.zeros((7, 1, n, 2))
+    nodes = grid.poly_order + 1
+    planes = np.zeros((7, 1, n, nodes))
     sl = slice(off, off + len(coeffs.s11))
-    for i, arr in enumerate((coeffs.s11, coeffs.s12, coeffs.s22, coeffs.f1, coeffs.f2)):
+    fields = (coeffs.s11, coeffs.s12, coeffs.s22, coeffs.f1, coeffs.f2)
+    if nodes != 2:   # the m-node solve stores phi / d_x with its element blocks
+        fields += (coeffs.phi, coeffs.bottom.d_x)
+    for i, arr in enumerate(fields):
         planes[i, 0, sl] = arr
     flags = np.zeros(n, dtype=bool)
     for e0, e1 in ranges:
         flags[e0:e1 + 1] = True
-    m = D.upload_members(D.member_record(grid, _FlatPack(), None, coeffs.dt))
+    m = D.upload_members(D.member_record(grid, _FlatPack(), None, coeffs.dt,
+                                         any_order=nodes != 2))
     cp = D.dev(planes)
     fb = D.dev(D.flags_to_bits(flags[None]).view(np.int32), dtype=np.int32)
     orr = D.dev(outer_right[None])
     T = D.torch()
-    p = T.zeros((1, n, 2), dtype=T.float64, device="cuda")
-    hu = T.zeros((1, n, 2), dtype=T.float64, device="cuda")
+    p = T.zeros((1, n, nodes), dtype=T.float64, device="cuda")
+    hu = T.zeros((1, n, nodes), dtype=T.float64, device="cuda")
     st = D.new_status(1)
-    _lib.check(lib.nh_ldg_solve(D.ptr(m), 1, n, D.ptr(cp), D.ptr(fb), D.ptr(orr), coeffs.rho,
-                                flux.c11, flux.c12, flux.c22, D.ptr(p), D.ptr(hu), D.ptr(st),
-                                D.stream_ptr()), "nh_ldg_solve")
+    if nodes != 2:
+        ws = D.pm_workspace(nodes, 1, n)
+        _lib.check(lib.nh_pm_ldg_solve(D.ptr(m), D.ptr(D.upload_members(D.pm_record(grid))),
+                                       nodes, 1, n, D.ptr(cp), D.ptr(fb), D.ptr(orr),
+                                       coeffs.rho, flux.c11, flux.c12, flux.c22, D.ptr(p),
+                                       D.ptr(hu), D.ptr(st), D.ptr(ws), ws.numel(),
+                                       D.stream_ptr()), "nh_pm_ldg_solve")
+    else:
+        _lib.check(lib.nh_ldg_solve(D.ptr(m), 1, n, D.ptr(cp), D.ptr(fb), D.ptr(orr),
+                                    coeffs.rho, flux.c11, flux.c12, flux.c22, D.ptr(p),
+                                    D.ptr(hu), D.ptr(st), D.stream_ptr()), "nh_ldg_solve")
     status = D.read_status(st)
     D.raise_for_status(status, 0.0, 0.0)
     return p[0].cpu().numpy(), hu[0].cpu().numpy()
@@ -210,23 +231,32 @@ def correct_momentum(predictor: FlowState, sol: PressureSolution,
     off = coeffs.offset
     if lo - off < 0 or hi + 1 - off > len(coeffs.phi):
         raise ValueError("coefficient window does not cover the solved ranges")
-    planes = np.zeros((7, 1, n, 2))
+    nodes = grid.poly_order + 1
+    planes = np.zeros((7, 1, n, nodes))
     sl = slice(off, off + len(coeffs.phi))
     planes[5, 0, sl] = coeffs.phi
     planes[6, 0, sl] = coeffs.bottom.d_x
     flags = np.zeros(n, dtype=bool)
     for e0, e1 in sol.ranges:
         flags[e0:e1 + 1] = True
-    m = D.upload_members(D.member_record(grid, _FlatPack(), None, coeffs.dt))
+    m = D.upload_members(D.member_record(grid, _FlatPack(), None, coeffs.dt,
+                                         any_order=nodes != 2))
     h = D.dev(predictor.h.values[None])
     p = D.dev(sol.p_nh.values[None])
     hw = D.dev(predictor.hw.values[None])
     out = D.torch().empty_like(hw)
     cp = D.dev(planes)
     fb = D.dev(D.flags_to_bits(flags[None]).view(np.int32), dtype=np.int32)
-    _lib.check(lib.nh_correct_momentum(D.ptr(m), 1, n, D.ptr(h), D.ptr(p), D.ptr(cp), D.ptr(fb),
-                                       coeffs.rho, D.ptr(hw), D.ptr(out), D.stream_ptr()),
-               "nh_correct_momentum")
+    if nodes != 2:
+        _lib.check(lib.nh_pm_correct_momentum(D.ptr(m),
+                                              D.ptr(D.upload_members(D.pm_record(grid))), nodes,
+                                              1, n, D.ptr(h), D.ptr(p), D.ptr(cp), D.ptr(fb),
+                                              coeffs.rho, D.ptr(hw), D.ptr(out),
+                                              D.stream_ptr()), "nh_pm_correct_momentum")
+    else:
+        _lib.check(lib.nh_correct_momentum(D.ptr(m), 1, n, D.ptr(h), D.ptr(p), D.ptr(cp),
+                                           D.ptr(fb), coeffs.rho, D.ptr(hw), D.ptr(out),
+                                           D.stream_ptr()), "nh_correct_momentum")
     return FlowState._wrap(predictor.h, sol.hu_corrected,
                            NodalField._wrap(grid, out[0].cpu().numpy()), predictor.time)
 

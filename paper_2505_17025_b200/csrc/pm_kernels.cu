@@ -64,6 +64,8 @@ struct PmArgs {
   double* gauge_h;
   int n_gauges;
   const uint32_t* given;   // NH_MODE_CORRECT_GIVEN: [B][ceil(N/32)] ranges to correct
+  const double* coef;      // coefficient-level calls: [7][B*N*M] s11 s12 s22 f1 f2 phi d_x
+  const double* outer_right;   // coefficient-level solve: [B][N] hu right of each element
   int step;
   int corr;         // the step has a correction (mode != hydrostatic)
   nh_scheme sch;
@@ -362,46 +364,30 @@ __device__ __forceinline__ bool gauss_jordan(double (&A)[2 * M][2 * M + 3]) {
   return ok;
 }
 
+__device__ __forceinline__ bool given_flag(const PmArgs& a, int b, int e) {
+  return (a.given[(size_t)b * ((a.N + 31) / 32) + (e >> 5)] >> (e & 31)) & 1u;
+}
+
+__device__ __forceinline__ void store_super_pm(const PmArgs& a, int idx, const Super& S) {
+  const size_t BN = (size_t)a.B * a.N;
+  a.sup[idx] = S.ga; a.sup[BN + idx] = S.aa; a.sup[2 * BN + idx] = S.ba;
+  a.sup[3 * BN + idx] = S.gz; a.sup[4 * BN + idx] = S.az; a.sup[5 * BN + idx] = S.bz;
+}
+
+// One flagged element's 2M x 2M LDG block (unknowns interleaved P0, Q0, P1,
+// Q1, ... as the reference's template, corrector.py:187-203, values
+// :329-336) eliminated to its super-element; the solution columns go to rec
+// for the reconstruction, phi / d_x to pdx for the hw update.
 template <int M>
-__global__ void __launch_bounds__(PTB) pm_condense(PmArgs a) {
-  const int idx = blockIdx.x * PTB + threadIdx.x;
-  if (idx >= a.B * a.N) return;
-  const int N = a.N, b = idx / N, e = idx - b * N;
-  const size_t BN = (size_t)a.B * N, o = (size_t)idx * M;
-  if (!a.flags[idx]) {   // outside every range: a_e = 0, z_e = uncorrected hu at node 0
-    const Super S = super_gap(a.hu_out[o]);
-    a.sup[idx] = S.ga; a.sup[BN + idx] = S.aa; a.sup[2 * BN + idx] = S.ba;
-    a.sup[3 * BN + idx] = S.gz; a.sup[4 * BN + idx] = S.az; a.sup[5 * BN + idx] = S.bz;
-    return;
-  }
-  const nh_member& m = a.members[b];
-  const nh_pm_member& c = a.pm[b];
-  const nh_scheme& sch = a.sch;
-  const Elem<M> q = load_elem<M>(a.h_out, a.hu_out, a.hw_out, o);
-  // coefficients at the predictor's time: t + dt in a step, the given state's
-  // own time for apply_correction
-  const BottomTime bt1 = bottom_time(m, a.given ? a.time[b] : a.time[b] + m.dt);
-  const LdgConst lk = make_ldg_const(m.dt, sch.g, sch.rho);
-  Chan ch[M];
-  double eta[M], hx[M], ex[M];
-#pragma unroll
-  for (int j = 0; j < M; ++j) {
-    const Bottom6 bb = bottom_all(m, bt1, node_x<M>(m, c, e, j));
-    ch[j] = Chan{bb.d, bb.d_x, bb.d_t, bb.d_tt, bb.d_xt, bb.d_xx};
-    eta[j] = q.h[j] - bb.d;
-  }
-  ederiv_m<M>(m, c, q.h, hx);
-  ederiv_m<M>(m, c, eta, ex);
-  NodeCoef nc[M];
-#pragma unroll
-  for (int j = 0; j < M; ++j) nc[j] = ldg_coefficients(q.h[j], q.q[j], q.w[j], hx[j], ex[j], ch[j], lk);
-  // element block, unknowns interleaved (P0, Q0, P1, Q1, ...) as the
-  // reference's template (corrector.py:187-203, values :329-336)
+__device__ __forceinline__ void condense_block(const PmArgs& a, const nh_pm_member& c,
+                                               const NodeCoef (&nc)[M], const double (&dxb)[M],
+                                               int b, int e, int idx, bool range_end) {
+  const size_t BN = (size_t)a.B * a.N;
   constexpr int R = 2 * M;
   double A[R][R + 3];
   const double* Mm = c.mass;
   const double* K = c.stiffness;
-  const double rho = sch.rho, inv_rho = lk.inv_rho, c11 = sch.c11;
+  const double rho = a.sch.rho, inv_rho = 1.0 / rho, c11 = a.sch.c11;
 #pragma unroll
   for (int i = 0; i < M; ++i) {
 #pragma unroll
@@ -424,7 +410,6 @@ __global__ void __launch_bounds__(PTB) pm_condense(PmArgs a) {
   //   left : P row -a_{e-1};  Q row -(Q0 + c11 (a_{e-1} - P0))
   //   right: P row +P_last (inside a range; p* = 0 at a range end);
   //          Q row +(z_{e+1} + c11 P_last)
-  const bool range_end = (e == N - 1) || !a.flags[idx + 1];
   A[1][1] -= 1.0;
   A[1][0] += c11;
   if (!range_end) A[R - 2][R - 2] += 1.0;
@@ -438,8 +423,7 @@ __global__ void __launch_bounds__(PTB) pm_condense(PmArgs a) {
   S.gz = fma(-c11, A[0][R], A[1][R]);
   S.az = fma(-c11, A[0][R + 1], A[1][R + 1]);
   S.bz = fma(-c11, A[0][R + 2], A[1][R + 2]);
-  a.sup[idx] = S.ga; a.sup[BN + idx] = S.aa; a.sup[2 * BN + idx] = S.ba;
-  a.sup[3 * BN + idx] = S.gz; a.sup[4 * BN + idx] = S.az; a.sup[5 * BN + idx] = S.bz;
+  store_super_pm(a, idx, S);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     a.rec[(size_t)(3 * r) * BN + idx] = A[r][R];
@@ -449,7 +433,102 @@ __global__ void __launch_bounds__(PTB) pm_condense(PmArgs a) {
 #pragma unroll
   for (int j = 0; j < M; ++j) {
     a.pdx[(size_t)j * BN + idx] = nc[j].phi;
-    a.pdx[(size_t)(M + j) * BN + idx] = ch[j].d_x;
+    a.pdx[(size_t)(M + j) * BN + idx] = dxb[j];
+  }
+}
+
+// LDG coefficients of one element from its state at bottom time bt
+// (corrector.py:100-170 per node: the P1 ldg_coefficients)
+template <int M>
+__device__ __forceinline__ void element_coefficients(const nh_member& m, const nh_pm_member& c,
+                                                     const BottomTime& bt, const LdgConst& lk,
+                                                     const Elem<M>& q, int e, NodeCoef (&nc)[M],
+                                                     double (&dxb)[M]) {
+  Chan ch[M];
+  double eta[M], hx[M], ex[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    const Bottom6 bb = bottom_all(m, bt, node_x<M>(m, c, e, j));
+    ch[j] = Chan{bb.d, bb.d_x, bb.d_t, bb.d_tt, bb.d_xt, bb.d_xx};
+    eta[j] = q.h[j] - bb.d;
+    dxb[j] = bb.d_x;
+  }
+  ederiv_m<M>(m, c, q.h, hx);
+  ederiv_m<M>(m, c, eta, ex);
+#pragma unroll
+  for (int j = 0; j < M; ++j) nc[j] = ldg_coefficients(q.h[j], q.q[j], q.w[j], hx[j], ex[j], ch[j], lk);
+}
+
+template <int M>
+__global__ void __launch_bounds__(PTB) pm_condense(PmArgs a) {
+  const int idx = blockIdx.x * PTB + threadIdx.x;
+  if (idx >= a.B * a.N) return;
+  const int N = a.N, b = idx / N, e = idx - b * N;
+  const size_t o = (size_t)idx * M;
+  if (!a.flags[idx]) {   // outside every range: a_e = 0, z_e = uncorrected hu at node 0
+    store_super_pm(a, idx, super_gap(a.hu_out[o]));
+    return;
+  }
+  const nh_member& m = a.members[b];
+  const nh_pm_member& c = a.pm[b];
+  const Elem<M> q = load_elem<M>(a.h_out, a.hu_out, a.hw_out, o);
+  // coefficients at the predictor's time: t + dt in a step, the given state's
+  // own time for apply_correction
+  const BottomTime bt1 = bottom_time(m, a.given ? a.time[b] : a.time[b] + m.dt);
+  NodeCoef nc[M];
+  double dxb[M];
+  element_coefficients<M>(m, c, bt1, make_ldg_const(m.dt, a.sch.g, a.sch.rho), q, e, nc, dxb);
+  condense_block<M>(a, c, nc, dxb, b, e, idx, (e == N - 1) || !a.flags[idx + 1]);
+}
+
+// coefficient-level solve (ldg_solve / solve_on_ranges): the element blocks
+// from given coefficient planes and flags; a gap element's z is the outer
+// trace right of its left neighbour
+template <int M>
+__global__ void __launch_bounds__(PTB) pm_condense_coef(PmArgs a) {
+  const int idx = blockIdx.x * PTB + threadIdx.x;
+  if (idx >= a.B * a.N) return;
+  const int N = a.N, b = idx / N, e = idx - b * N;
+  const size_t BNM = (size_t)a.B * N * M, o = (size_t)idx * M;
+  const bool f = given_flag(a, b, e);
+  a.flags[idx] = f ? 1 : 0;
+  if (!f) {
+    store_super_pm(a, idx, super_gap(e > 0 ? a.outer_right[idx - 1] : 0.0));
+    return;
+  }
+  NodeCoef nc[M];
+  double dxb[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    nc[j].s11 = a.coef[o + j];
+    nc[j].s12 = a.coef[BNM + o + j];
+    nc[j].s22 = a.coef[2 * BNM + o + j];
+    nc[j].f1 = a.coef[3 * BNM + o + j];
+    nc[j].f2 = a.coef[4 * BNM + o + j];
+    nc[j].phi = a.coef[5 * BNM + o + j];
+    dxb[j] = a.coef[6 * BNM + o + j];
+  }
+  condense_block<M>(a, a.pm[b], nc, dxb, b, e, idx, (e == N - 1) || !given_flag(a, b, e + 1));
+}
+
+// coefficient planes of assemble_coefficients / phi_term at the state's time
+template <int M>
+__global__ void __launch_bounds__(PTB) pm_coef_kernel(PmArgs a, double* coef) {
+  const int idx = blockIdx.x * PTB + threadIdx.x;
+  if (idx >= a.B * a.N) return;
+  const int N = a.N, b = idx / N, e = idx - b * N;
+  const nh_member& m = a.members[b];
+  const size_t BNM = (size_t)a.B * N * M, o = (size_t)idx * M;
+  const Elem<M> q = load_elem<M>(a.h_in, a.hu_in, a.hw_in, o);
+  NodeCoef nc[M];
+  double dxb[M];
+  element_coefficients<M>(m, a.pm[b], bottom_time(m, a.time[b]),
+                          make_ldg_const(m.dt, a.sch.g, a.sch.rho), q, e, nc, dxb);
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    coef[o + j] = nc[j].s11; coef[BNM + o + j] = nc[j].s12; coef[2 * BNM + o + j] = nc[j].s22;
+    coef[3 * BNM + o + j] = nc[j].f1; coef[4 * BNM + o + j] = nc[j].f2;
+    coef[5 * BNM + o + j] = nc[j].phi; coef[6 * BNM + o + j] = dxb[j];
   }
 }
 
@@ -473,8 +552,13 @@ __global__ void __launch_bounds__(PTB) pm_chain(PmArgs a) {
       a.chain[2 * BN + k] = mm; a.chain[3 * BN + k] = nn;
     }
     // outer trace right of the member: the right ghost of hu (corrector.py:400-402)
-    const double qn = a.hu_out[(base + N - 1) * M + M - 1];
-    double z = m.bc_right == NH_BC_WALL ? -qn : qn;
+    double z;
+    if (a.outer_right) {
+      z = a.outer_right[base + N - 1];
+    } else {
+      const double qn = a.hu_out[(base + N - 1) * M + M - 1];
+      z = m.bc_right == NH_BC_WALL ? -qn : qn;
+    }
     for (int e = N - 1; e >= 0; --e) {
       const size_t k = base + e;
       a.io[BN + k] = z;
@@ -525,11 +609,11 @@ template <int M>
 __global__ void __launch_bounds__(PTB) pm_correct(PmArgs a) {
   const int idx = blockIdx.x * PTB + threadIdx.x;
   if (idx >= a.B * a.N) return;
-  if (!a.flags[idx]) return;
   const int N = a.N, b = idx / N, e = idx - b * N;
+  if (a.flags ? !a.flags[idx] : !given_flag(a, b, e)) return;
   const nh_member& m = a.members[b];
   const nh_pm_member& c = a.pm[b];
-  const size_t BN = (size_t)a.B * N, o = (size_t)idx * M;
+  const size_t BN = (size_t)a.B * N, BNM = BN * M, o = (size_t)idx * M;
   double hp[M], hx[M];
 #pragma unroll
   for (int j = 0; j < M; ++j) hp[j] = a.h_out[o + j] * a.p[o + j];
@@ -551,7 +635,8 @@ __global__ void __launch_bounds__(PTB) pm_correct(PmArgs a) {
   const double cdt = m.dt / a.sch.rho;
 #pragma unroll
   for (int j = 0; j < M; ++j) {
-    const double phi = a.pdx[(size_t)j * BN + idx], dx = a.pdx[(size_t)(M + j) * BN + idx];
+    const double phi = a.coef ? a.coef[5 * BNM + o + j] : a.pdx[(size_t)j * BN + idx];
+    const double dx = a.coef ? a.coef[6 * BNM + o + j] : a.pdx[(size_t)(M + j) * BN + idx];
     const double quad = 4.0 + dx * dx;
     const double bp = nh_div(6.0, quad) * a.p[o + j] + nh_div(dx, quad) * hx[j] + phi;
     a.hw_out[o + j] += cdt * bp;
@@ -670,6 +755,29 @@ int pm_advance_m(PmArgs a, int n_steps, double** A, double** Bb, const nh_output
 
 size_t pm_doubles(int m, size_t BN) { return BN * (size_t)(18 * m + 12); }
 
+// workspace partition (nh_pm_workspace_bytes); returns the ping-pong state
+double* carve(PmArgs& a, void* workspace, int m, int B, int N, int*& hw_any) {
+  const size_t BN = (size_t)B * N, BNM = BN * m;
+  double* w = (double*)workspace;
+  double* alt = w;            w += 3 * BNM;
+  a.k1 = w;                   w += 3 * BNM;
+  a.qs = w;                   w += 3 * BNM;
+  a.sup = w;                  w += 6 * BN;
+  a.rec = w;                  w += 6 * (size_t)m * BN;
+  a.pdx = w;                  w += 2 * (size_t)m * BN;
+  a.chain = w;                w += 4 * BN;
+  a.io = w;                   w += 2 * BN;
+  a.p = w;                    w += BNM;
+  uint8_t* u8 = (uint8_t*)w;
+  a.raw = u8;
+  a.flags = u8 + BN;
+  hw_any = (int*)(((uintptr_t)(u8 + 2 * BN) + 15) & ~(uintptr_t)15);
+  return alt;
+}
+
+template <class F>
+void* by_m(int m, F f2, F f3, F f4) { return m == 2 ? f2 : m == 3 ? f3 : f4; }
+
 }  // namespace
 
 extern "C" {
@@ -696,22 +804,10 @@ int nh_pm_advance(const nh_member* members, const nh_pm_member* pm, int m, int B
   if (n_steps == 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t BN = (size_t)B * N, BNM = BN * m;
-  double* w = (double*)workspace;
   PmArgs a;
   std::memset(&a, 0, sizeof a);
-  double* alt = w;            w += 3 * BNM;
-  a.k1 = w;                   w += 3 * BNM;
-  a.qs = w;                   w += 3 * BNM;
-  a.sup = w;                  w += 6 * BN;
-  a.rec = w;                  w += 6 * (size_t)m * BN;
-  a.pdx = w;                  w += 2 * (size_t)m * BN;
-  a.chain = w;                w += 4 * BN;
-  a.io = w;                   w += 2 * BN;
-  a.p = w;                    w += BNM;
-  uint8_t* u8 = (uint8_t*)w;
-  a.raw = u8;
-  a.flags = u8 + BN;
-  int* hw_any = (int*)(((uintptr_t)(u8 + 2 * BN) + 15) & ~(uintptr_t)15);
+  int* hw_any = nullptr;
+  double* alt = carve(a, workspace, m, B, N, hw_any);
   const bool wcrit = sc.mode == NH_MODE_ADAPTIVE &&
                      (sc.criterion == NH_CRIT_W || sc.criterion == NH_CRIT_W_X);
   if (cudaMemsetAsync(a.raw, 0, BN, s) != cudaSuccess) return NH_E_CUDA;
@@ -767,6 +863,70 @@ int nh_pm_criterion(const nh_member* members, const nh_pm_member* pm, int m, int
   void* k = m == 2 ? (void*)pm_crit_kernel<2> : m == 3 ? (void*)pm_crit_kernel<3>
                                                         : (void*)pm_crit_kernel<4>;
   return launch(k, B * N, args, (cudaStream_t)stream);
+}
+
+int nh_pm_coefficients(const nh_member* members, const nh_pm_member* pm, int m, int B, int N,
+                       const double* h, const double* hu, const double* hw, const double* time,
+                       double g, double rho, double* coef, void* stream) {
+  if (!members || !pm || !h || !hu || !hw || !time || !coef) return NH_E_ARG;
+  if (m < 2 || m > NH_PM_MAX_NODES || B < 1 || N < 2) return NH_E_ARG;
+  PmArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.members = members; a.pm = pm; a.h_in = h; a.hu_in = hu; a.hw_in = hw;
+  a.time = const_cast<double*>(time); a.B = B; a.N = N; a.sch.g = g; a.sch.rho = rho;
+  void* args[2] = {&a, &coef};
+  return launch(by_m(m, (void*)pm_coef_kernel<2>, (void*)pm_coef_kernel<3>,
+                     (void*)pm_coef_kernel<4>), B * N, args, (cudaStream_t)stream);
+}
+
+int nh_pm_ldg_solve(const nh_member* members, const nh_pm_member* pm, int m, int B, int N,
+                    const double* coef, const uint32_t* flags, const double* outer_right,
+                    double rho, double c11, double c12, double c22, double* p, double* hu,
+                    nh_status* status, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!members || !pm || !coef || !flags || !outer_right || !p || !hu || !status || !workspace)
+    return NH_E_ARG;
+  if (m < 2 || m > NH_PM_MAX_NODES || B < 1 || N < 2) return NH_E_ARG;
+  if (workspace_bytes < nh_pm_workspace_bytes(m, B, N)) return NH_E_ARG;
+  if (c12 != -0.5 || c22 != 0.0) return NH_E_UNSUPPORTED;
+  cudaStream_t s = (cudaStream_t)stream;
+  PmArgs a;
+  std::memset(&a, 0, sizeof a);
+  int* hw_any = nullptr;
+  carve(a, workspace, m, B, N, hw_any);
+  a.members = members; a.pm = pm; a.status = status; a.B = B; a.N = N;
+  a.coef = coef; a.given = flags; a.outer_right = outer_right; a.corr = 1;
+  a.sch.rho = rho; a.sch.c11 = c11; a.sch.c12 = c12; a.sch.c22 = c22;
+  a.hu_out = hu;
+  a.p = p;
+  a.time = nullptr;
+  void* args[1] = {&a};
+  int rc = launch(by_m(m, (void*)pm_condense_coef<2>, (void*)pm_condense_coef<3>,
+                       (void*)pm_condense_coef<4>), B * N, args, s);
+  if (!rc) rc = launch(by_m(m, (void*)pm_chain<2>, (void*)pm_chain<3>, (void*)pm_chain<4>), B,
+                       args, s);
+  if (!rc) rc = launch(by_m(m, (void*)pm_reconstruct<2>, (void*)pm_reconstruct<3>,
+                            (void*)pm_reconstruct<4>), B * N, args, s);
+  return rc;
+}
+
+int nh_pm_correct_momentum(const nh_member* members, const nh_pm_member* pm, int m, int B, int N,
+                           const double* h, const double* p, const double* coef,
+                           const uint32_t* flags, double rho, const double* hw, double* hw_out,
+                           void* stream) {
+  if (!members || !pm || !h || !p || !coef || !flags || !hw || !hw_out) return NH_E_ARG;
+  if (m < 2 || m > NH_PM_MAX_NODES || B < 1 || N < 2) return NH_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = (size_t)B * N * m * 8;
+  if (hw_out != hw && cudaMemcpyAsync(hw_out, hw, bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return NH_E_CUDA;
+  PmArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.members = members; a.pm = pm; a.B = B; a.N = N;
+  a.h_out = const_cast<double*>(h); a.p = const_cast<double*>(p); a.hw_out = hw_out;
+  a.coef = coef; a.given = flags; a.flags = nullptr; a.sch.rho = rho;
+  void* args[1] = {&a};
+  return launch(by_m(m, (void*)pm_correct<2>, (void*)pm_correct<3>, (void*)pm_correct<4>), B * N,
+                args, s);
 }
 
 }  // extern "C"

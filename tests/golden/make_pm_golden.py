@@ -113,6 +113,21 @@ def run_case(name, spec, out):
         out[f"{name}_corr_ranges"] = np.array(CORR[name])
         out[f"{name}_corr_hu"], out[f"{name}_corr_hw"] = cst.hu.values, cst.hw.values
         out[f"{name}_corr_p"] = sol.p_nh.values
+        # the coefficient-level functions on the same predictor (corrector.py:100-482)
+        from nhswe.corrector import (assemble_coefficients, correct_momentum, ldg_solve,
+                                     solve_on_ranges)
+        co = assemble_coefficients(st, bathy, spec["dt"])
+        out[f"{name}_coef"] = np.stack([co.s11, co.s12, co.s22, co.f1, co.f2, co.phi])
+        lo, hi = CORR[name][0][0], CORR[name][-1][1]
+        cw = assemble_coefficients(st, bathy, spec["dt"], window=slice(lo, hi + 1))
+        out[f"{name}_coefw"] = np.stack([cw.s11, cw.s12, cw.s22, cw.f1, cw.f2, cw.phi])
+        e0, e1 = CORR[name][0]
+        pl, hl = ldg_solve(co, (e0, e1), outer_hu=(0.0, 0.37))
+        out[f"{name}_ldg_p"], out[f"{name}_ldg_hu"] = pl, hl
+        sol2 = solve_on_ranges(st, co, CORR[name], bcs)
+        out[f"{name}_sor_p"], out[f"{name}_sor_hu"] = sol2.p_nh.values, sol2.hu_corrected.values
+        cm = correct_momentum(st, sol2, co)
+        out[f"{name}_cm_hw"] = cm.hw.values
     print(f"{name}: {spec['steps']} steps, flagged per step {counts[:3]}...{counts[-3:]}, "
           f"|hw| {np.abs(st.hw.values).max():.3e}")
 

@@ -154,3 +154,29 @@ def test_apply_correction_given_ranges_high_order(name):
     assert rel(st.hu.values, GOLD[f"{name}_corr_hu"]) <= 1e-10
     assert rel(st.hw.values, GOLD[f"{name}_corr_hw"]) <= 1e-10
     assert rel(sol.p_nh.values, GOLD[f"{name}_corr_p"]) <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["p2_flat_adaptive", "p3_plate_global"])
+def test_coefficient_level_functions_high_order(name):
+    """assemble_coefficients (full grid and a window), ldg_solve on one range
+    with an outer trace, solve_on_ranges and correct_momentum at p = 2, 3
+    against the reference's (corrector.py:100-482)."""
+    s, grid, bathy, bcs, _, _ = setup(name)
+    pred = P.FlowState(P.NodalField(grid, GOLD[f"{name}_h"]), P.NodalField(grid, GOLD[f"{name}_hu"]),
+                       P.NodalField(grid, GOLD[f"{name}_hw"]), float(GOLD[f"{name}_t"]))
+    ranges = [tuple(r) for r in GOLD[f"{name}_corr_ranges"].tolist()]
+    co = P.assemble_coefficients(pred, bathy, s["dt"])
+    for k, f in enumerate(("s11", "s12", "s22", "f1", "f2", "phi")):
+        ref = GOLD[f"{name}_coef"][k]
+        assert np.abs(getattr(co, f) - ref).max() <= 1e-12 * max(np.abs(ref).max(), 1e-300), f
+    lo, hi = ranges[0][0], ranges[-1][1]
+    cw = P.assemble_coefficients(pred, bathy, s["dt"], window=slice(lo, hi + 1))
+    assert cw.offset == lo and cw.s11.shape == GOLD[f"{name}_coefw"][0].shape
+    p, hu = P.ldg_solve(co, ranges[0], outer_hu=(0.0, 0.37))
+    assert rel(p, GOLD[f"{name}_ldg_p"]) <= 1e-10 and rel(hu, GOLD[f"{name}_ldg_hu"]) <= 1e-10
+    sol = P.solve_on_ranges(pred, co, ranges, bcs)
+    assert rel(sol.p_nh.values, GOLD[f"{name}_sor_p"]) <= 1e-10
+    assert rel(sol.hu_corrected.values, GOLD[f"{name}_sor_hu"]) <= 1e-10
+    cm = P.correct_momentum(pred, sol, co)
+    assert cm.h is pred.h
+    assert rel(cm.hw.values, GOLD[f"{name}_cm_hw"]) <= 1e-10
