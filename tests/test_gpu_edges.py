@@ -33,7 +33,7 @@ def test_member_sizes_at_tile_boundaries(n, mode):
     L = [10.0, 7.0]
     bcs = [P.BoundaryPair(P.WALL, P.ABSORBING), P.BoundaryPair(P.ABSORBING, P.WALL)]
     grids = [P.GridSpec(0.0, l, n) for l in L]
-    dts = [0.05 * g.dx, 0.04 * g.dx]
+    dts = [0.05 * grids[0].dx, 0.04 * grids[1].dx]
     recs = np.concatenate([D.member_record(g, P.FlatBottom(1.0), b, dt)
                            for g, b, dt in zip(grids, bcs, dts)])
     st = [bump_state(g, 0.2, 0.4 * g.x_right, 0.8) for g in grids]
