@@ -396,6 +396,10 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
     if (cudaFuncSetAttribute(nh_stream_kernel(0), cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)nh_stream_kp_smem()) != cudaSuccess)
       return NH_E_CUDA;
+    if (void* kf = nh_stream_kp_fused_ptr())
+      if (cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)nh_stream_kp_smem()) != cudaSuccess)
+        return NH_E_CUDA;
     ks_grid = std::max(1, nks) * sms;
     kc_grid = std::max(1, nkc) * sms;
     if (getenv("NH_STREAM_VERBOSE"))
@@ -431,7 +435,12 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   void* kc = nh_stream_kernel(2);
   void* ks = nh_stream_kernel(3);
   const bool corr = sc.mode != NH_MODE_HYDROSTATIC;
-  const bool fused_ks = nh_stream_kp_fuses_ks() != 0;
+  // global mode: every tile is condensed, so K_P does it in the same pass
+  // (no K_S launch, no state re-read); NH_KP_FUSE_GLOBAL=0 keeps K_S
+  static const bool fuse_global =
+      !getenv("NH_KP_FUSE_GLOBAL") || atoi(getenv("NH_KP_FUSE_GLOBAL")) != 0;
+  const bool fused_ks = fuse_global && sc.mode == NH_MODE_GLOBAL && nh_stream_kp_fused_ptr();
+  void* kp_step = fused_ks ? nh_stream_kp_fused_ptr() : kp;
   {
     void* args[1] = {&a};
     if (int rc = stream_launch(nh_stream_kernel(4), 5, dim3((B + 255) / 256), dim3(256), args, s))
@@ -457,7 +466,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   auto launch_step = [&](int k, cudaStream_t st) -> int {
     set_step(k);
     void* args[1] = {&a};
-    int rc = stream_launch(kp, 0, gp, bpp, args, st, kp_smem);
+    int rc = stream_launch(kp_step, 0, gp, bpp, args, st, kp_smem);
     if (!rc && a.n_gauges > 0)
       rc = stream_launch(nh_stream_kernel(6), 5, dim3((unsigned)(((size_t)B * a.n_gauges + 127) / 128)),
                          dim3(128), args, st);

@@ -22,9 +22,11 @@ __global__ void __launch_bounds__(TP2, NH_KP2_MIN_BLOCKS) nh_stream_kp(StreamArg
 }
 size_t nh_stream_kp_smem() { return sizeof(Kp2Smem); }
 int nh_stream_kp_threads() { return TP2; }
+void* nh_stream_kp_fused_ptr() { return nullptr; }
 #else
 
-__global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(StreamArgs a) {
+template <bool FUSE>
+__device__ __forceinline__ void kp_entry(const StreamArgs& a) {
   __shared__ nh_member msh;
   __shared__ MemberConst mc;
   extern __shared__ __align__(16) unsigned char kp_dyn[];   // KpSmem (dynamic: > 48 KB at 512 threads)
@@ -35,8 +37,17 @@ __global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(Stream
   int b = blockIdx.z * 65535 + blockIdx.y;
   if (b >= a.B) return;   // padding of the (tiles, 65535, z) grid
   if (a.order) b = a.order[b];
-  kp_tile(a, tile_idx(a, b, blockIdx.x), msh, mc, ks);
+  kp_tile<FUSE>(a, tile_idx(a, b, blockIdx.x), msh, mc, ks);
 }
+
+__global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp(StreamArgs a) {
+  kp_entry<false>(a);
+}
+// K_P with the K_S condensation fused in (global mode)
+__global__ void __launch_bounds__(TPB, NH_STREAM_MIN_BLOCKS) nh_stream_kp_fused(StreamArgs a) {
+  kp_entry<true>(a);
+}
+void* nh_stream_kp_fused_ptr() { return (void*)nh_stream_kp_fused; }
 
 size_t nh_stream_kp_smem() { return sizeof(KpSmem); }
 int nh_stream_kp_threads() { return TPB; }
@@ -44,4 +55,4 @@ int nh_stream_kp_threads() { return TPB; }
 
 void* nh_stream_kp_ptr() { return (void*)nh_stream_kp; }
 int nh_stream_kp_records_hw_any() { return NH_KP_E2 ? 0 : 1; }   // w / w_x fallback (K_F)
-int nh_stream_kp_fuses_ks() { return (NH_KP_FUSE_KS && !NH_KP_E2) ? 1 : 0; }
+

@@ -189,10 +189,11 @@ __device__ __forceinline__ Super tile_up(Super agg, bool tflag, double* wnode, d
 
 }  // namespace
 
-#ifndef NH_KP_FUSE_KS
-#define NH_KP_FUSE_KS 0   // 1: K_P also condenses its flagged tiles (no K_S launch); measured slower
-                          // (config 4 adaptive K_P+K_S 0.77 -> 0.86 ms: register pressure on every tile)
-#endif
+// FUSE (template argument of the K_P body): K_P also condenses its flagged
+// tiles and K_S is not launched.  Used for the global mode, where every tile
+// is condensed and the fusion saves K_S's state re-read (config 4 global step
+// 2.30 -> 2.17 ms); the adaptive mode keeps K_S (fused: 0.82 -> 0.86 ms,
+// register pressure on every tile).
 
 // ---------------------------------------------------------------------- K_P
 struct KpSmem {
@@ -281,7 +282,7 @@ __device__ __forceinline__ void load_member(const StreamArgs& a, int b, nh_membe
         reinterpret_cast<const unsigned long long*>(a.mconst + (size_t)b * 16)[i - MW];
 }
 
-// One flagged element's LDG condensation (K_S, or K_P with NH_KP_FUSE_KS):
+// One flagged element's LDG condensation (K_S, or the fused K_P):
 // LDG coefficients at t + dt (corrector.py:100-170), the element block
 // eliminated to its super-element (corrector.py:173-349 -> physics.cuh), the
 // super-element + reconstruction rows stored for K_C, and phi / d_x stored in
@@ -315,7 +316,7 @@ __device__ __forceinline__ void condense_element(const StreamArgs& a, const nh_m
   pn[2 * BN] = c0.phi; pn[3 * BN] = c1.phi; pn[4 * BN] = b0.d_x; pn[5 * BN] = b1.d_x;
 }
 
-template <int KIND, class SM>
+template <int KIND, bool FUSE, class SM>
 __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
                                         const MemberConst& mc, const TileIdx& ti, Q6 q,
                                         SM& ks, double* sq) {
@@ -500,8 +501,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
         a.tile_list[atomicAdd(a.tile_count, 1)] = b * T + tile;   // work list of K_S / K_C
       }
     }
-#if NH_KP_FUSE_KS
-    if (nf) {   // CTA-uniform: this tile's condensation and aggregate (K_S's work)
+    if (FUSE && nf) {   // CTA-uniform: this tile's condensation and aggregate (K_S's work)
       Super S = super_identity();
       if (own) S = super_gap(qp.q0);
       if (flag) condense_element<KIND>(a, m, mc.lk, mc.bt1, b, e, qp, (e == N - 1) || !eff(i + 1), S);
@@ -510,7 +510,6 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
       Super v = tile_up(S, flag, kss.wnode, kss.wagg, kss.bnode, kss.wflag, lane, ti.warp);
       if (i == 0) store_super(a.tile_agg + ((size_t)b * T + tile) * 8, v);
     }
-#endif
     // right-end ghost outer trace (corrector.py:400-402)
     if (e == N - 1 && own) {
       double qq = qp.q1;
@@ -525,7 +524,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
 // NH_HP_TRACES(ks), made visible by the caller's barrier.
 // hw += dt/rho (6/quad p + d_x/quad (h p)_x + phi) on flagged elements
 // (corrector.py:441-482); (h p)_x lifts use the neighbours' (h p) traces.
-template <class SM>
+template <bool FUSE, class SM>
 __device__ __forceinline__ void kp_correct_and_step(const StreamArgs& a, const TileIdx& ti,
                                                     const nh_member& msh, const MemberConst& mc,
                                                     SM& ks, double* sq, Q6 q, bool f, double p0,
@@ -577,19 +576,20 @@ __device__ __forceinline__ void kp_correct_and_step(const StreamArgs& a, const T
     if (__syncthreads_or(ti.own && (q.w0 != 0.0 || q.w1 != 0.0)) && i == 0) a.hw_any[b] = 1;
   }
 #if NH_KP_RUNTIME_KIND
-  kp_body<-1>(a, msh, mc, ti, q, ks, sq);
+  kp_body<-1, FUSE>(a, msh, mc, ti, q, ks, sq);
 #else
   switch (msh.bottom_kind) {
-    case NH_BOTTOM_FLAT: kp_body<NH_BOTTOM_FLAT>(a, msh, mc, ti, q, ks, sq); break;
-    case NH_BOTTOM_PLATE: kp_body<NH_BOTTOM_PLATE>(a, msh, mc, ti, q, ks, sq); break;
-    case NH_BOTTOM_QUARTIC_SLIDE: kp_body<NH_BOTTOM_QUARTIC_SLIDE>(a, msh, mc, ti, q, ks, sq); break;
-    case NH_BOTTOM_SMOOTH_BOX: kp_body<NH_BOTTOM_SMOOTH_BOX>(a, msh, mc, ti, q, ks, sq); break;
-    default: kp_body<NH_BOTTOM_SLOPE_SLIDE>(a, msh, mc, ti, q, ks, sq); break;
+    case NH_BOTTOM_FLAT: kp_body<NH_BOTTOM_FLAT, FUSE>(a, msh, mc, ti, q, ks, sq); break;
+    case NH_BOTTOM_PLATE: kp_body<NH_BOTTOM_PLATE, FUSE>(a, msh, mc, ti, q, ks, sq); break;
+    case NH_BOTTOM_QUARTIC_SLIDE: kp_body<NH_BOTTOM_QUARTIC_SLIDE, FUSE>(a, msh, mc, ti, q, ks, sq); break;
+    case NH_BOTTOM_SMOOTH_BOX: kp_body<NH_BOTTOM_SMOOTH_BOX, FUSE>(a, msh, mc, ti, q, ks, sq); break;
+    default: kp_body<NH_BOTTOM_SLOPE_SLIDE, FUSE>(a, msh, mc, ti, q, ks, sq); break;
   }
 #endif
 }
 
-// One K_P tile (b, tile): the body of nh_stream_kp.
+// One K_P tile (b, tile): the body of nh_stream_kp / nh_stream_kp_fused.
+template <bool FUSE>
 __device__ __forceinline__ void kp_tile(const StreamArgs& a, const TileIdx& ti, nh_member& msh,
                                         MemberConst& mc, KpSmem& ks) {
   const int N = a.N, i = ti.i, b = ti.b, e = ti.e;
@@ -616,5 +616,5 @@ __device__ __forceinline__ void kp_tile(const StreamArgs& a, const TileIdx& ti, 
     NH_HP_TRACES(ks)[1 * TPB + i] = q.h1 * p1;
   }
   __syncthreads();
-  kp_correct_and_step(a, ti, msh, mc, ks, ks.sq, q, f, p0, p1, phi0, phi1, dx0, dx1);
+  kp_correct_and_step<FUSE>(a, ti, msh, mc, ks, ks.sq, q, f, p0, p1, phi0, phi1, dx0, dx1);
 }
