@@ -297,10 +297,11 @@ def run_b200(args):
     # launches with a CUDA event between consecutive kernels on the launching
     # stream (nh_stream_timing)
     ktimes, ms_ev = {}, None
+    ksteps = args.kernel_steps if args.kernel_steps > 0 else args.steps
     if path == "stream":
         D.stream_timing(True)
         ev0.record()
-        ens.advance(args.steps, args.mode, crit, path=path)
+        ens.advance(ksteps, args.mode, crit, path=path)
         ev1.record()
         ev1.synchronize()
         ms_ev = ev0.elapsed_time(ev1)
@@ -316,7 +317,7 @@ def run_b200(args):
     bad = np.flatnonzero(st["error_key"] != _lib.STATUS_OK_KEY)
     errors = {"count": int(bad.size),
               "first": [[int(i), *decode_error(st["error_key"][i])] for i in bad[:4]]}
-    steps_run = args.steps * (2 if ms_ev is not None else 1)   # both timed regions
+    steps_run = args.steps + (ksteps if ms_ev is not None else 0)   # both timed regions
     frac = float(st["flagged"].sum()) / (B * N * max(steps_run, 1))
     cells = B * N * args.steps * world
     value = cells / (ms * 1e-3)
@@ -329,7 +330,7 @@ def run_b200(args):
         kp_avg, kp_n, kname = ms / max(args.steps, 1), args.steps, "nh_step_kernel (per step)"
     # cells per K_P launch: the whole ensemble, or one member block when it is
     # run in blocks (config 5 at full size)
-    kp_bytes = BYTES_PER_CELL_STEP * B * N * args.steps / max(kp_n, 1)
+    kp_bytes = BYTES_PER_CELL_STEP * B * N * (ksteps if path == "stream" else args.steps) / max(kp_n, 1)
     achieved = kp_bytes / (kp_avg * 1e-3) / 1e9
     traffic, traffic_src = _kp_traffic()
     if traffic_src and traffic_src.get("workload", "config4") != args.workload:
@@ -399,7 +400,7 @@ def run_b200(args):
                          "algorithmic_bytes_per_launch": kp_bytes,
                          "peak_kind": peak_kind,
                          "traffic_source": traffic_src.get("source") if traffic_src else None,
-                         "event_timed_ms_per_step": (ms_ev / args.steps) if ms_ev else None,
+                         "event_timed_ms_per_step": (ms_ev / ksteps) if ms_ev else None,
                          "note": "algorithmic 96 B/cell (state read + write) x B*N cells per "
                                  "launch / event-timed launch (timed region 2: the K steps after "
                                  "the headline region, plain launches with CUDA events between "
@@ -426,6 +427,8 @@ def main():
     ap.add_argument("--mode", default="adaptive", choices=["adaptive", "global"])
     ap.add_argument("--cpu-steps", type=int, default=1000)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--kernel-steps", type=int, default=0,
+                    help="steps of timed region 2 (per-kernel events); default: --steps")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
