@@ -400,6 +400,9 @@ def run_b200(args):
                          "algorithmic_bytes_per_launch": kp_bytes,
                          "peak_kind": peak_kind,
                          "traffic_source": traffic_src.get("source") if traffic_src else None,
+                         # the binding resource of K_P in the same ncu capture
+                         "ncu_fp64_pipe_active_pct": (traffic_src or {}).get("fp64_pipe_active_pct"),
+                         "ncu_issue_active_pct": (traffic_src or {}).get("issue_active_pct"),
                          "event_timed_ms_per_step": (ms_ev / ksteps) if ms_ev else None,
                          "note": "algorithmic 96 B/cell (state read + write) x B*N cells per "
                                  "launch / event-timed launch (timed region 2: the K steps after "

@@ -30,13 +30,19 @@ def main(rep, pattern, out):
             "dram_read_bytes": val("dram__bytes_read.sum", scale),
             "dram_write_bytes": val("dram__bytes_write.sum", scale),
             "duration_ms": val("gpu__time_duration.sum", tscale),
+            # the compute side of the roofline (K_P is fp64-issue bound)
+            "fp64_pipe_pct": float(d.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+                                         "nan").replace(",", "")),
+            "issue_active_pct": float(d.get("smsp__issue_active.avg.pct_of_peak_sustained_active",
+                                            "nan").replace(",", "")),
         })
     r0 = recs[0]
     res = {"source": rep.split("/")[-1], "workload": "config4", "kernel": r0["kernel"], "grid": r0["grid"],
            "block": r0["block"],
            "dram_bytes_per_launch": r0["dram_read_bytes"] + r0["dram_write_bytes"],
            "dram_read_bytes": r0["dram_read_bytes"], "dram_write_bytes": r0["dram_write_bytes"],
-           "ncu_duration_ms": r0["duration_ms"], "launches_captured": len(recs)}
+           "ncu_duration_ms": r0["duration_ms"], "launches_captured": len(recs),
+           "fp64_pipe_active_pct": r0["fp64_pipe_pct"], "issue_active_pct": r0["issue_active_pct"]}
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
 
