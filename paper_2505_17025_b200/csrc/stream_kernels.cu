@@ -242,7 +242,8 @@ __device__ __forceinline__ void kc_tile(const StreamArgs& a, int bt, KcSmem& kc)
   const bool valid = e >= 0 && e < N;
   const bool own = valid && i >= H && i < H + OWN;
   const size_t o = ((size_t)b * N + (valid ? e : 0)) * 2;
-  const bool flag = own && a.flags_cur[(size_t)b * N + e];
+  // global mode flags every element: no dependent flag load before the scratch loads
+  const bool flag = own && (a.sch.mode == NH_MODE_GLOBAL || a.flags_cur[(size_t)b * N + e]);
   Super S = super_identity();
   double R[6] = {0, 0, 0, 0, 0, 0};
   if (flag) {

@@ -50,8 +50,8 @@ def test_sweep_matches_reference_table(name, tmp_path):
     for i, r in enumerate(rows):
         for j, c in enumerate(cols):
             v, rv = r[c], ref[i, j]
-            if c == "time_ratio":
-                assert 0.0 < v < 10.0
+            if c == "time_ratio":   # a timing, not a parity column: positive and finite
+                assert 0.0 < v < 100.0
                 continue
             if np.isnan(rv):
                 assert v == "", (r["criterion"], r["enlarge"], c)
