@@ -57,6 +57,93 @@ __device__ __forceinline__ void ks_body(const StreamArgs& a, int bt, const nh_me
   if (i == 0) store_super(a.tile_agg + ((size_t)b * T + tile) * 8, v);
 }
 
+#ifndef NH_KS_WARP
+#define NH_KS_WARP 1   // 1: one warp per tile, no CTA barriers (0: one CTA per tile)
+#endif
+
+#if NH_KS_WARP
+// One warp per tile: the tile's NW slices of 32 elements one after another,
+// each reduced by the same warp tree as tile_up's per-warp level, then the
+// slice aggregates by tile_up's cross-warp tree -- the same merges in the same
+// order, so the tile aggregate is bitwise the CTA version's, without a CTA
+// barrier: the warps of a CTA work on different tiles independently.
+struct KsWarpSmem {
+  nh_member msh;
+  MemberConst mc;
+  double wnode[31 * 6];
+  double wagg[NW * 6];
+};
+
+template <int KIND>
+__device__ __forceinline__ void ks_warp_tile(const StreamArgs& a, int bt, KsWarpSmem& ws, int lane) {
+  const int N = a.N, T = a.tiles;
+  const int b = bt / T, tile = bt % T;
+  const nh_member& m = ws.msh;
+  for (int c = 0; c < NW; ++c) {
+    const int i = c * 32 + lane;
+    const int e = tile * OWN - H + i;
+    const bool valid = e >= 0 && e < N;
+    const bool own = valid && i >= H && i < H + OWN;
+    const size_t o = ((size_t)b * N + (valid ? e : 0)) * 2;
+    const size_t fe = (size_t)b * N + (valid ? e : 0);
+    const bool flag = own && a.flags_cur[fe];
+    Super S = super_identity();
+    if (own) S = super_gap(a.hu_out[o]);
+    if (flag) {
+      double2 vh = *reinterpret_cast<const double2*>(a.h_out + o);
+      double2 vq = *reinterpret_cast<const double2*>(a.hu_out + o);
+      double2 vw = *reinterpret_cast<const double2*>(a.hw_out + o);
+      const bool range_end = (e == N - 1) || !a.flags_cur[fe + 1];
+      condense_element<KIND>(a, m, ws.mc.lk, ws.mc.bt1, b, e, Q6{vh.x, vh.y, vq.x, vq.y, vw.x, vw.y},
+                             range_end, S);
+    }
+    Super agg = S;   // tile_up's per-warp level
+    if (__any_sync(0xffffffffu, flag)) {
+      agg = warp_up(agg, ws.wnode, lane, 5);
+    } else {
+      unsigned nonid = __ballot_sync(0xffffffffu, !is_identity(agg));
+      int first = nonid ? __ffs(nonid) - 1 : 0;
+      agg = shfl_super(agg, first);
+      if (!nonid) agg = super_identity();
+    }
+    if (lane == 0) store_super(ws.wagg + c * 6, agg);
+    __syncwarp();
+  }
+  Super v = lane < NW ? load_super(ws.wagg + lane * 6) : super_identity();
+  v = warp_up(v, ws.wnode, lane, 3);   // tile_up's cross-warp level
+  if (lane == 0) store_super(a.tile_agg + ((size_t)b * T + tile) * 8, v);
+}
+
+__global__ void __launch_bounds__(TPB, NH_KS_MIN_BLOCKS) nh_stream_ks(StreamArgs a) {
+  __shared__ KsWarpSmem wsm[NW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  KsWarpSmem& ws = wsm[warp];
+  const bool all = a.sch.mode == NH_MODE_GLOBAL;
+  const int n = all ? a.B * a.tiles : *a.tile_count;
+  constexpr int MW = (int)(sizeof(nh_member) / 8);
+  for (int w = blockIdx.x * NW + warp; w < n; w += gridDim.x * NW) {
+    const int bt = all ? w : a.tile_list[w];
+    const int b = bt / a.tiles;
+    __syncwarp();   // the previous tile's reads of the member record are done
+    for (int k = lane; k < MW + 16; k += 32) {
+      if (k < MW)
+        reinterpret_cast<unsigned long long*>(&ws.msh)[k] =
+            reinterpret_cast<const unsigned long long*>(a.members + b)[k];
+      else
+        reinterpret_cast<unsigned long long*>(&ws.mc)[k - MW] =
+            reinterpret_cast<const unsigned long long*>(a.mconst + (size_t)b * 16)[k - MW];
+    }
+    __syncwarp();
+    switch (ws.msh.bottom_kind) {
+      case NH_BOTTOM_FLAT: ks_warp_tile<NH_BOTTOM_FLAT>(a, bt, ws, lane); break;
+      case NH_BOTTOM_PLATE: ks_warp_tile<NH_BOTTOM_PLATE>(a, bt, ws, lane); break;
+      case NH_BOTTOM_QUARTIC_SLIDE: ks_warp_tile<NH_BOTTOM_QUARTIC_SLIDE>(a, bt, ws, lane); break;
+      case NH_BOTTOM_SMOOTH_BOX: ks_warp_tile<NH_BOTTOM_SMOOTH_BOX>(a, bt, ws, lane); break;
+      default: ks_warp_tile<NH_BOTTOM_SLOPE_SLIDE>(a, bt, ws, lane); break;
+    }
+  }
+}
+#else
 // Persistent: the grid strides over the step's list of flagged tiles (or over
 // every tile in global mode, where all are flagged and the list is skipped).
 __global__ void __launch_bounds__(TPB, NH_KS_MIN_BLOCKS) nh_stream_ks(StreamArgs a) {
@@ -80,6 +167,7 @@ __global__ void __launch_bounds__(TPB, NH_KS_MIN_BLOCKS) nh_stream_ks(StreamArgs
     __syncthreads();   // shared memory is reused by the next tile
   }
 }
+#endif
 
 // ---------------------------------------------------------------------- K_X
 // One warp per member: chain of its T tile aggregates (lane l folds tiles
