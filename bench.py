@@ -1,36 +1,44 @@
 #!/usr/bin/env python
-"""Benchmark: cell-steps/s of the fused adaptive NH-SWE step on B200.
+"""Benchmark: cell-steps/s of the adaptive NH-SWE step on B200.
 
-Workload (N=1): BASELINE config 4 -- 4096 members x 4096 P1 elements, fp64,
-adaptive mask (|eta/d| > 1e-3), mixed solitary / box-uplift members.  A
-"step" is one time step of every member.  W untimed warm-up steps, then K
-timed steps of the streaming path (four kernels per step: K_P predictor +
-criterion, K_S condensation, K_X tile chain, K_C reconstruction; the 805 MB
-state is far larger than the 126 MB L2, so every step streams it from HBM).
+Workload (N=1): BASELINE config 5 -- 65536 landslide members x 16384 P1
+elements, fp64, adaptive mask (|eta/d| > 1e-3), the largest configuration
+BASELINE runs on one GPU.  A "step" is one time step of every member.  The
+ensemble starts from rest, so `--spinup` untimed steps first carry it into
+its flagged regime, then W untimed warm-up steps, then K timed
+steps of the streaming path (K_P predictor + criterion, K_S condensation,
+K_X tile chain, K_C reconstruction; the 51.5 GB state is far larger than the
+126 MB L2, so every step streams it from HBM).
 
-Roofline: the dominant kernel is K_P.  Its algorithmic traffic is the state
-read + write, 96 B per cell; its average launch time is
-measured live with CUDA events recorded between the launches inside the
-timed region (nh_stream_timing), and `traffic` is the DRAM bytes per K_P
-launch from the committed `ncu --set full` capture (profiles/kp_traffic.json).
+Legs of one run (all on the same ensemble, one after the other):
+  value     K steps, the CUDA-graph time loop as the library runs it
+  roofline  the next K steps with CUDA events between the kernels: K_P's
+            average launch time -> algorithmic GB/s (96 B per cell)
+  global    --global-steps steps in global mode on the same state (the
+            reference's paired adaptive/global timing, cli.py:259-267)
+  e2e       K steps through driver.advance_host from pinned HOST memory:
+            copy-in, compute and copy-out pipelined over member blocks
+  cpu       the reference's own step (nhswe from baseline/_ref) on the host
+            cores, one sampled member per process (rank 0, N=1 only)
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--workload config4|config5] [--mode adaptive|global]
+                    [--workload config5|config4] [--mode adaptive|global]
 
-Multi-GPU (torchrun, one process per GPU): members are sharded over ranks
-with no collective on the step path (weak scaling: every rank steps its own
-4096-member shard); time = max over ranks of the device-timed region.
+Multi-GPU (torchrun, one process per GPU): config 5 is sharded evenly over
+the ranks with parallel.shard (a member's parameters depend on its index
+only, so the shards together are exactly the N=1 ensemble; "scaling":
+"strong"), no collective on the step path; time = max over ranks of the
+device-timed region; an untimed gather_summaries collects per-member results.
 
---impl reference times the CPU oracle port (oracle/nhswe_oracle.py, the
-restatement of the reference's numpy/LAPACK step, bit-exact with it) on all
-host cores: one member per process, each advancing K steps.
+--impl reference times the reference's own adaptive_step (the unmodified
+package installed into baseline/_ref) on the host cores, one member per
+process over a bounded sample of the same workload window.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -42,25 +50,24 @@ sys.path.insert(0, ROOT)
 
 BYTES_PER_CELL_STEP = 96          # read + write of 6 fp64 state values
 METRIC = "cell-steps/sec (ensemble x cells x steps) incl. NH correction"
+SPINUP = {"config5": 1000, "config4": 0}
 
 
-def _kp_traffic():
-    """DRAM bytes (read + write) per K_P launch from the committed ncu capture."""
+def _profile_json(name):
     try:
-        with open(os.path.join(ROOT, "profiles", "kp_traffic.json")) as f:
-            d = json.load(f)
-        return float(d["dram_bytes_per_launch"]), d
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
     except Exception:
-        return None, None
+        return None
 
 
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), float(p.get("sm_max_mhz", 1965.0)), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
     except Exception:
-        return 6650.0, 1965.0, "fallback"
+        return 7672.0, "fallback (B200_PROFILING.md)"
 
 
 # ------------------------------------------------------------------ clocks
@@ -75,19 +82,20 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.lines = []
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)   # first sample before the region starts
         except Exception:
             self.proc = None
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -100,7 +108,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
+        for l in self.lines:
             f = [x.strip() for x in l.split(",")]
             if len(f) < 7:
                 continue
@@ -119,22 +127,26 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ workloads
 
-def build_workload(name: str, rank: int, world: int):
-    """Member table + device initial state for this rank's shard."""
-    import numpy as np
-    import torch
+def get_config(name: str, **kw):
     from paper_2505_17025_b200 import configs
-    from paper_2505_17025_b200._device import dev
-    if name == "config4":
-        per = 4096
-        cfg = configs.Config4(n_members=per * world)
-        idx = range(rank * per, (rank + 1) * per)
-    else:
-        cfg = configs.Config5()
-        per = cfg.n_members // world
-        idx = range(rank * per, (rank + 1) * per)
-    recs = cfg.records(list(idx))
-    h, hu, hw = init_device(cfg, recs, list(idx))
+    return configs.Config5(**kw) if name == "config5" else configs.Config4(**kw)
+
+
+def workload_members(name: str, rank: int, world: int, members=None, **kw):
+    """(config, member indices, nh_member records) of this rank's shard:
+    parallel.shard of the workload's members, or the given indices.  A
+    member's record depends on its index only, so the shards of any world
+    size concatenate to the N=1 table (tests/test_parallel.py)."""
+    from paper_2505_17025_b200.parallel import shard
+    cfg = get_config(name, **kw)
+    idx = list(members) if members is not None else list(shard(cfg.n_members, world, rank))
+    return cfg, idx, cfg.records(idx)
+
+
+def build_workload(name: str, rank: int, world: int, members=None):
+    """Member table + device initial state of this rank's shard."""
+    cfg, idx, recs = workload_members(name, rank, world, members)
+    h, hu, hw = init_device(cfg, recs, idx)
     return cfg, recs, h, hu, hw
 
 
@@ -144,7 +156,7 @@ def init_device(cfg, recs, idx):
     import numpy as np
     import torch
     from paper_2505_17025_b200 import _lib
-    from paper_2505_17025_b200._device import dev, ptr, require_cuda, stream_ptr, upload_members
+    from paper_2505_17025_b200._device import ptr, require_cuda, stream_ptr, upload_members
     from paper_2505_17025_b200.configs import solitary_state
     lib = require_cuda()
     B, N = len(idx), cfg.n_elements
@@ -187,47 +199,69 @@ def init_device(cfg, recs, idx):
     return h, hu, hw
 
 
-# ------------------------------------------------------------------ CPU baseline
+# ------------------------------------------------------------------ CPU legs
 
 def _cpu_worker(args):
-    wl, i, n_steps, mode = args
+    """One member through the reference's own adaptive_step: `spin` untimed
+    steps (the same workload window as the GPU legs), then `n_steps` timed."""
+    wl, i, spin, n_steps, mode = args
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     from threadpoolctl import threadpool_limits
-    import numpy as np
-    from oracle import nhswe_oracle as O
-    from paper_2505_17025_b200 import configs
-    from tests.helpers import oracle_depth, oracle_member
     with threadpool_limits(1):
-        cfg = configs.Config4(n_members=max(4096, i + 1)) if wl == "config4" else configs.Config5()
-        m = cfg.member(i)
-        h, hu, hw = cfg.host_state(i, oracle_depth)
-        mem = oracle_member(m.grid, m.bathymetry, m.bcs, m.dt)
-        O.step(mem, h, hu, hw, 0.0, mode)        # warm caches / lru templates
+        cfg = get_config(wl)
+        try:
+            from tests.harness.ref_bridge import reference_member
+            R, grid, bathy, bcs, dt, st = reference_member(cfg, i)
+            crit = R.Criterion("eta_over_d") if mode == "adaptive" else None
+            kind = "reference"
+
+            def step(s):
+                return R.adaptive_step(s, dt, bathy, bcs, mode=mode, crit=crit,
+                                       cfl_warn=False).state
+        except Exception:
+            # the reference is not installed: the oracle port (bit-exact restatement)
+            from oracle import nhswe_oracle as O
+            from tests.helpers import oracle_depth, oracle_member
+            m = cfg.member(i)
+            mem = oracle_member(m.grid, m.bathymetry, m.bcs, m.dt)
+            h, hu, hw = cfg.host_state(i, oracle_depth)
+            st = (h, hu, hw, 0.0)
+            kind = "port"
+
+            def step(s):
+                r = O.step(mem, s[0], s[1], s[2], s[3], mode)
+                return (r.h, r.hu, r.hw, r.time)
+        for _ in range(spin):
+            st = step(st)
         t0 = time.perf_counter()
-        r = O.run(mem, h, hu, hw, n_steps, mode=mode)
-        dt = time.perf_counter() - t0
-    return cfg.n_elements * n_steps, dt, r.fraction_mean
+        for _ in range(n_steps):
+            st = step(st)
+        dt_s = time.perf_counter() - t0
+    return cfg.n_elements * n_steps, dt_s, kind
 
 
-def cpu_baseline(workload: str, mode: str, n_steps: int, procs: int | None = None):
-    """Oracle port on the host cores: one member per process, n_steps each."""
+def cpu_sample(workload: str, mode: str, spin: int, n_steps: int, procs: int | None = None):
+    """The reference's step on the host cores: one member per process."""
     import multiprocessing as mp
     procs = procs or min(os.cpu_count() or 1, 32)
-    jobs = [(workload, 2 * k + (k % 2), n_steps, mode) for k in range(procs)]
-    ctx = mp.get_context("spawn")
+    cfg = get_config(workload)
+    stride = max(1, cfg.n_members // procs)
+    jobs = [(workload, k * stride + (k % 2), spin, n_steps, mode) for k in range(procs)]
     t0 = time.perf_counter()
-    with ctx.Pool(procs) as pool:
+    with mp.get_context("spawn").Pool(procs) as pool:
         res = pool.map(_cpu_worker, jobs)
     wall = time.perf_counter() - t0
     cells = sum(r[0] for r in res)
     slowest = max(r[1] for r in res)
-    return {"value": cells / slowest, "unit": "cell-steps/s", "cores": procs, "kind": "port",
-            "sample": f"{procs} members of {workload} (one per process, BLAS 1 thread), "
-                      f"{n_steps} {mode} steps each; rate = cells x steps / slowest process",
-            "wall_s": wall, "slowest_s": slowest, "mask_fraction": statistics.mean(r[2] for r in res)}
+    kind = res[0][2]
+    who = ("the reference's own adaptive_step (nhswe, baseline/_ref)" if kind == "reference"
+           else "the oracle port (reference not installed)")
+    return {"value": cells / slowest, "unit": "cell-steps/s", "cores": procs, "kind": kind,
+            "sample": f"{procs} members of {workload} (one per process, BLAS 1 thread) through "
+                      f"{who}: {spin} untimed spin-up steps, then {n_steps} timed {mode} steps "
+                      f"each; rate = cells x steps / slowest process",
+            "ms_per_member_step": 1e3 * slowest / n_steps, "wall_s": wall, "slowest_s": slowest}
 
-
-# ------------------------------------------------------------------ arms
 
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
@@ -238,24 +272,28 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if world > 1 and rank != 0:
         return
-    n_steps = args.steps
-    base = cpu_baseline(args.workload, args.mode, n_steps)
-    from paper_2505_17025_b200 import configs
-    cfg = configs.Config4() if args.workload == "config4" else configs.Config5()
+    spin = args.spinup + args.warmup
+    base = cpu_sample(args.workload, args.mode, spin, args.steps)
+    cfg = get_config(args.workload)
     line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "cell-steps/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            # one whole-workload step (all members) at the sampled rate
-            "ms_per_step": 1e3 * cfg.n_members * cfg.n_elements / base["value"],
-            "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            # the timed sample's own step time (every process advances its
+            # member by one step in parallel)
+            "ms_per_step": base["ms_per_member_step"],
+            "ms_per_step_full_workload_extrapolated":
+                1e3 * cfg.n_members * cfg.n_elements / base["value"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": args.workload, "mode": args.mode,
                        "members": cfg.n_members, "cells_per_member": cfg.n_elements,
-                       "sample": base["sample"]},
+                       "spinup_steps": args.spinup, "sample": base["sample"]},
             "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": base["value"], "unit": "cell-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
+
+# ------------------------------------------------------------------ GPU arm
 
 def run_b200(args):
     import numpy as np
@@ -264,25 +302,34 @@ def run_b200(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        tdist.init_process_group("nccl")
-    from paper_2505_17025_b200 import Criterion, Ensemble, _lib
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2505_17025_b200 import Criterion, Ensemble, _lib, parallel
     from paper_2505_17025_b200 import _device as D
-    from paper_2505_17025_b200._device import read_status
+    from paper_2505_17025_b200._device import decode_error, read_status
+    from paper_2505_17025_b200.driver import advance_host
     cfg, recs, h, hu, hw = build_workload(args.workload, rank, world)
     B, N = h.shape[0], h.shape[1]
     crit = Criterion("eta_over_d", 1e-3, False)
     ens = Ensemble(recs, h, hu, hw)
-    # warm-up steps (untimed)
-    ens.advance(args.warmup, args.mode, crit)
+    if args.spinup:
+        ens.advance(args.spinup, args.mode, crit)
+    ens.advance(args.warmup, args.mode, crit)      # warm-up steps (untimed)
     torch.cuda.synchronize()
     ens.reset_status()
-    # the state after the warm-up, in pinned host memory: the e2e leg below
-    # runs the same K steps as timed region 1 from the host (same window of
-    # the workload, so the two numbers differ only by the API and transfers)
-    host0 = None
-    if args.e2e and B * N * 48 <= 16e9:
-        host0 = [x.cpu().pin_memory() for x in (ens.h, ens.hu, ens.hw, ens.time)]
     path = ens.choose_path(args.mode, crit)
+    # the state after the warm-up, in pinned host memory, for the e2e leg
+    # (the same window of the workload as timed region 1)
+    host0, e2e_note = None, None
+    if args.e2e:
+        import psutil
+        need = B * N * 48 + B * 8
+        if psutil.virtual_memory().available > 1.25 * need:
+            host0 = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+                     for x in (ens.h, ens.hu, ens.hw, ens.time)]
+            for dst, src in zip(host0, (ens.h, ens.hu, ens.hw, ens.time)):
+                dst.copy_(src)
+        else:
+            e2e_note = f"host RAM below 1.25 x {need / 1e9:.1f} GB of state"
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         tdist.barrier()
@@ -296,127 +343,129 @@ def run_b200(args):
         ens.advance(args.steps, args.mode, crit, path=path)
         ev1.record()
         ev1.synchronize()
-    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        tdist.barrier()
     torch.cuda.synchronize()
+    ms = parallel.max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
     launches = D.launch_count() - n_launch0
+    st1 = read_status(ens.status)
+    frac = float(st1["flagged"].sum()) / (B * N * args.steps)
     # timed region 2 (roofline and kernel shares): the next K steps as plain
     # launches with a CUDA event between consecutive kernels on the launching
     # stream (nh_stream_timing)
     ktimes, ms_ev = {}, None
     ksteps = args.kernel_steps if args.kernel_steps > 0 else args.steps
-    if path == "stream":
-        D.stream_timing(True)
+    D.stream_timing(True)
+    ev0.record()
+    ens.advance(ksteps, args.mode, crit, path=path)
+    ev1.record()
+    ev1.synchronize()
+    ms_ev = ev0.elapsed_time(ev1)
+    ktimes = D.stream_kernel_times()
+    D.stream_timing(False)
+    # global mode on the same ensemble (paired timing, reference cli.py:259-267)
+    glob = None
+    if args.global_steps > 0 and args.mode == "adaptive":
+        torch.cuda.synchronize()
         ev0.record()
-        ens.advance(ksteps, args.mode, crit, path=path)
+        ens.advance(args.global_steps, "global", None, path=path)
         ev1.record()
         ev1.synchronize()
-        ms_ev = ev0.elapsed_time(ev1)
-        ktimes = D.stream_kernel_times()
-        D.stream_timing(False)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        ms = float(t.item())
+        gms = parallel.max_over_ranks(ev0.elapsed_time(ev1), device="cuda") / args.global_steps
+        glob = {"ms_per_step": gms, "value": B * N * world / (gms * 1e-3),
+                "steps": args.global_steps,
+                "global_over_adaptive_step_time": gms / (ms / args.steps)}
     st = read_status(ens.status)
     ok = bool((st["error_key"] == _lib.STATUS_OK_KEY).all())
-    from paper_2505_17025_b200._device import decode_error
     bad = np.flatnonzero(st["error_key"] != _lib.STATUS_OK_KEY)
     errors = {"count": int(bad.size),
               "first": [[int(i), *decode_error(st["error_key"][i])] for i in bad[:4]]}
-    steps_run = args.steps + (ksteps if ms_ev is not None else 0)   # both timed regions
-    frac = float(st["flagged"].sum()) / (B * N * max(steps_run, 1))
     cells = B * N * args.steps * world
     value = cells / (ms * 1e-3)
-    peak, _, peak_kind = _peaks()
-    if path == "stream":
-        kp_ms, kp_n = ktimes["nh_stream_kp"]
-        kp_avg = kp_ms / max(kp_n, 1)
-        kname = "nh_stream_kp"
-    else:   # resident path: one launch covers every step
-        kp_avg, kp_n, kname = ms / max(args.steps, 1), args.steps, "nh_step_kernel (per step)"
-    # cells per K_P launch: the whole ensemble, or one member block when it is
-    # run in blocks (config 5 at full size)
-    kp_bytes = BYTES_PER_CELL_STEP * B * N * (ksteps if path == "stream" else args.steps) / max(kp_n, 1)
+    peak, peak_kind = _peaks()
+    kp_ms, kp_n = ktimes["nh_stream_kp"]
+    kp_avg = kp_ms / max(kp_n, 1)
+    # cells per K_P launch: the whole shard, or one member block when the
+    # shard runs in blocks through one workspace
+    kp_bytes = BYTES_PER_CELL_STEP * B * N * ksteps / max(kp_n, 1)
     achieved = kp_bytes / (kp_avg * 1e-3) / 1e9
-    traffic, traffic_src = _kp_traffic()
-    if traffic_src and traffic_src.get("workload", "config4") != args.workload:
-        traffic, traffic_src = None, None     # the committed capture is of another shape
+    traffic_src = _profile_json(f"kp_traffic_{args.workload}.json")
+    traffic = None
+    if traffic_src:   # DRAM bytes per launch of the committed capture, per cell of this launch
+        traffic = traffic_src["dram_bytes_per_cell"] * kp_bytes / BYTES_PER_CELL_STEP
     shares = {k: {"ms_total": v[0], "launches": v[1], "share": v[0] / ms_ev}
               for k, v in ktimes.items() if v[1]}
 
-    # end to end through the public API: pinned host state -> device, K steps
-    # (Ensemble.advance -> nh_stream_advance), device -> pinned host, timed on
-    # the wall clock around synchronizes (the larger of wall and event time).
-    e2e = None
-    if args.e2e and B * N * 48 > 16e9:
-        e2e = {"skipped": "state larger than 16 GB; e2e host round trip measured on config4"}
-    elif args.e2e:
-        hh = host0
-        ho = [torch.empty_like(x).pin_memory() for x in hh[:3]]
+    # end to end through the public API: the post-warm-up state in pinned
+    # HOST memory -> driver.advance_host (member blocks: copy-in, K steps,
+    # copy-out, pipelined on three streams) -> host; wall clock around
+    # synchronizes, max over ranks
+    e2e = {"skipped": e2e_note} if e2e_note else None
+    if host0 is not None:
+        ens.release_workspace()   # advance_host streams through its own buffers
         torch.cuda.synchronize()
         if world > 1:
             tdist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         w0 = time.perf_counter()
-        e0.record()
-        dh = [x.to("cuda", non_blocking=True) for x in hh]   # h, hu, hw, time
-        ens2 = Ensemble(recs, *dh)
-        ens2.advance(args.steps, args.mode, crit)
-        for dst, src in zip(ho, (ens2.h, ens2.hu, ens2.hw)):
-            dst.copy_(src, non_blocking=True)
-        e1.record()
-        e1.synchronize()
-        ems = max(e0.elapsed_time(e1), (time.perf_counter() - w0) * 1e3)
-        if world > 1:
-            t = torch.tensor([ems], device="cuda")
-            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-            ems = float(t.item())
-        nbytes_in = sum(x.numel() * 8 for x in hh)
-        nbytes = sum(x.numel() * 8 for x in ho)
+        advance_host(recs, *host0, args.steps, args.mode, crit, block=args.e2e_block)
+        ems = parallel.max_over_ranks((time.perf_counter() - w0) * 1e3, device="cuda")
+        nbytes = sum(x.numel() * 8 for x in host0)
         e2e = {"value": cells / (ems * 1e-3), "unit": "cell-steps/s",
-               "h2d_bytes_per_step": nbytes_in / args.steps,
+               "h2d_bytes_per_step": nbytes / args.steps,
                "d2h_bytes_per_step": nbytes / args.steps,
-               "call": "Ensemble(host state + times -> HBM).advance(K) -> host state, one call "
-                       "per K steps, from the post-warm-up state (the K steps of region 1)"}
-        del dh, ens2, ho, host0
+               "ms": ems, "block_members": args.e2e_block,
+               "call": "driver.advance_host(pinned host h, hu, hw, time; K steps): member blocks "
+                       "copied in, stepped and copied out, pipelined on 3 CUDA streams; from the "
+                       "post-warm-up state (the K steps of region 1)"}
+        del host0
 
+    # per-member summaries on rank 0 (untimed; the only other collective)
+    summ = parallel.gather_summaries({"time": ens.time.cpu().numpy(),
+                                      "flagged": st["flagged"].astype(np.int64),
+                                      "ok": (st["error_key"] == _lib.STATUS_OK_KEY)})
     cpu = None
     if rank == 0 and world == 1 and args.cpu_steps > 0:
-        cpu = cpu_baseline(args.workload, args.mode, args.cpu_steps)
+        cpu = cpu_sample(args.workload, args.mode, args.spinup + args.warmup, args.cpu_steps)
     if rank == 0:
+        fp64 = _profile_json("fp64_peak.json") or {}
         line = {
             "metric": METRIC, "value": value, "unit": "cell-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": args.workload, "mode": args.mode, "members": B * world,
-                       "cells_per_member": N, "members_per_gpu": B,
-                       "criterion": "eta_over_d k_nh=1e-3", "mask_fraction": frac,
-                       "path": path,
-                       "l2": f"inputs > L2: state {B * N * 48 / 1e6:.0f} MB/GPU vs 126 MB L2, "
+            "config": {"workload": args.workload, "mode": args.mode,
+                       "members": int(len(summ["time"])), "cells_per_member": N,
+                       "members_per_gpu": B, "parallelism": f"member shards x{world}",
+                       "criterion": "eta_over_d k_nh=1e-3", "spinup_steps": args.spinup,
+                       "mask_fraction": frac, "path": path,
+                       "l2": f"inputs > L2: state {B * N * 48 / 1e9:.1f} GB/GPU vs 126 MB L2, "
                              "streamed every step",
                        "member_chunk": ens.stream_chunk() if path == "stream" else B,
-                       "status_ok": ok, "errors": errors},
+                       "status_ok": ok and bool(summ["ok"].all()), "errors": errors},
             "gpu_launches": launches,
             "time_loop": "CUDA graph of step pairs (nh_stream_advance), timed region 1",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak,
-                         "traffic": traffic if path == "stream" else None,
-                         "kernel": kname, "kernel_ms_avg": kp_avg, "kernel_launches": kp_n,
-                         "algorithmic_bytes_per_launch": kp_bytes,
-                         "peak_kind": peak_kind,
-                         "traffic_source": traffic_src.get("source") if traffic_src else None,
-                         # the binding resource of K_P in the same ncu capture
-                         "ncu_fp64_pipe_active_pct": (traffic_src or {}).get("fp64_pipe_active_pct"),
-                         "ncu_issue_active_pct": (traffic_src or {}).get("issue_active_pct"),
-                         "event_timed_ms_per_step": (ms_ev / ksteps) if ms_ev else None,
-                         "note": "algorithmic 96 B/cell (state read + write) x B*N cells per "
-                                 "launch / event-timed launch (timed region 2: the K steps after "
-                                 "the headline region, plain launches with CUDA events between "
-                                 "kernels); K_P is fp64-issue bound, not HBM bound (profiles/)"},
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "nh_stream_kp", "kernel_ms_avg": kp_avg,
+                         "kernel_launches": kp_n,
+                         "algorithmic_bytes_per_launch": kp_bytes, "peak_kind": peak_kind,
+                         "traffic_source": (traffic_src or {}).get("source"),
+                         "fp64": {"kp_fp64_pipe_active_pct":
+                                      (traffic_src or {}).get("fp64_pipe_active_pct"),
+                                  "kp_issue_active_pct": (traffic_src or {}).get("issue_active_pct"),
+                                  "measured_dfma_peak_tflops": fp64.get("tflops"),
+                                  "source": "ncu --set full of K_P (profiles/) and "
+                                            "profiles/fp64_peak.json"},
+                         "event_timed_ms_per_step": ms_ev / ksteps,
+                         "note": "algorithmic 96 B/cell (state read + write) x cells per launch / "
+                                 "event-timed launch (timed region 2: the K steps after the "
+                                 "headline region, plain launches with CUDA events between "
+                                 "kernels)"},
             "kernel_shares": shares,
             "clocks": clk.summary(),
         }
+        if glob:
+            line["global"] = glob
         if e2e:
             line["e2e"] = e2e
         if cpu:
@@ -429,16 +478,23 @@ def run_b200(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="config4", choices=["config4", "config5"])
+    ap.add_argument("--workload", default="config5", choices=["config5", "config4"])
     ap.add_argument("--mode", default="adaptive", choices=["adaptive", "global"])
-    ap.add_argument("--cpu-steps", type=int, default=1000)
+    ap.add_argument("--spinup", type=int, default=None,
+                    help="untimed steps before the warm-up (default: 1000 for config5, which "
+                         "starts from rest, 0 for config4)")
+    ap.add_argument("--global-steps", type=int, default=10)
+    ap.add_argument("--cpu-steps", type=int, default=200)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--e2e-block", type=int, default=4096)
     ap.add_argument("--kernel-steps", type=int, default=0,
                     help="steps of timed region 2 (per-kernel events); default: --steps")
     args = ap.parse_args()
+    if args.spinup is None:
+        args.spinup = SPINUP[args.workload]
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -25,7 +25,8 @@
 extern "C" {
 #endif
 
-#define NH_ABI_VERSION 3   /* 2: nh_outputs gauge fields; 3: nh_pm_* (orders p > 1), w / w_x on nh_stream_advance */
+#define NH_ABI_VERSION 4   /* 2: nh_outputs gauge fields; 3: nh_pm_* (orders p > 1), w / w_x on nh_stream_advance;
+                               4: residual gate (nh_scheme.residual_tol, nh_status resid_*) */
 
 /* bottom model kinds (reference bathymetry.py:66-184 + harness models) */
 #define NH_BOTTOM_FLAT 0          /* FlatBottom(h0)                         bathymetry.py:66-79   */
@@ -60,6 +61,10 @@ extern "C" {
 #define NH_ERR_POSITIVITY_STAGE2 3  /* _advance after stage 2: PositivityError(-1, t+dt)                */
 #define NH_ERR_SOLVE_NONFINITE 4    /* EllipticSolveError, corrector.py:356-357                        */
 #define NH_ERR_SOLVE_PIVOT 5        /* zero pivot in the condensed elimination (singular system)         */
+#define NH_ERR_SOLVE_RESIDUAL 6     /* EllipticSolveError: ||Ax-b|| / max(||b||, max|A| ||x||) of a
+                                       step's batched system above residual_tol, corrector.py:359-366  */
+#define NH_ERR_STRUCTURE 7          /* AssertionError: s12 > 0 violated at a flagged node,
+                                       corrector.py:70-74 (s11 + s21 = 0 holds by construction)     */
 
 /* launch / argument errors (return values) */
 #define NH_E_ARG (-1)
@@ -98,6 +103,9 @@ typedef struct nh_scheme {
     int32_t criterion;      /* NH_CRIT_*                                    */
     int32_t enlarge;        /* Criterion.enlarge                            */
     int32_t record_cfl;     /* track max advisory CFL (hydrostatic.py:199)  */
+    double residual_tol;    /* residual gate of every elliptic solve (corrector.py:297,
+                               359-366; the reference default is 1e-10); <= 0 disables the gate
+                               (the norms are still accumulated)                                */
 } nh_scheme;
 
 /* Per-member result record, written by the device. */
@@ -108,6 +116,10 @@ typedef struct nh_status {
     int64_t flagged;        /* flagged elements summed over the steps       */
     int32_t steps_done;
     int32_t any_hw;         /* any(hw != 0) of the output state (w/w_x fallback) */
+    double resid_max;       /* largest relative residual of the steps' elliptic solves
+                               (the reference's `rel`, corrector.py:359-362)          */
+    double resid_acc[4];    /* running sums of the current solve: ||Ax-b||^2, ||b||^2,
+                               ||x||^2 and max|A| (device scratch; zero between solves) */
 } nh_status;
 
 /* Optional outputs of nh_advance. */
@@ -275,13 +287,17 @@ int nh_coefficients(const nh_member* members, int n_members, int n_elements,
 /* LDG solve from given coefficients on flagged ranges, corrector._solve_batched
  * / ldg_solve / solve_on_ranges (corrector.py:292-424).  coef as above
  * (only s11, s12, s22, f1, f2 read), flags [B][ceil(N/32)] (ranges = maximal
- * runs), outer_right [B][N] = outer hu trace used when element e ends a range
- * (corrector.py:388-403).  Outputs p, hu [B][N][2] on flagged elements
- * (untouched elsewhere). */
+ * runs, split further where range_starts [B][ceil(N/32)] has a bit set, or
+ * NULL: adjacent ranges are separate systems, as in the reference's
+ * block-diagonal batch), outer_right [B][N] = outer hu trace used when
+ * element e ends a range (corrector.py:388-403).  Outputs p, hu [B][N][2] on
+ * flagged elements (untouched elsewhere).  The member's batched system is
+ * checked like corrector.py:355-366: status.resid_max = ||Ax-b|| /
+ * max(||b||, max|A| ||x||), NH_ERR_SOLVE_RESIDUAL above residual_tol (> 0). */
 int nh_ldg_solve(const nh_member* members, int n_members, int n_elements,
-                 const double* coef, const uint32_t* flags, const double* outer_right,
-                 double rho, double c11, double c12, double c22,
-                 double* p, double* hu, nh_status* status, void* stream);
+                 const double* coef, const uint32_t* flags, const uint32_t* range_starts,
+                 const double* outer_right, double rho, double c11, double c12, double c22,
+                 double residual_tol, double* p, double* hu, nh_status* status, void* stream);
 
 /* Vertical-momentum update from a solved pressure, corrector.correct_momentum
  * (corrector.py:441-482): hw_out = hw_in + dt/rho * bottom pressure on flagged

@@ -140,6 +140,12 @@ def raise_for_status(status: np.ndarray, t0, dt, member: int = 0):
         raise PositivityError(-1, t + dtm)
     if code == _lib.ERR_SOLVE_PIVOT:
         raise EllipticSolveError(f"singular elliptic system (zero pivot in element {element})")
+    if code == _lib.ERR_SOLVE_RESIDUAL:
+        raise EllipticSolveError(
+            f"elliptic solve residual {float(status['resid_max'][member]):.3e} exceeds the "
+            f"residual tolerance at t={t + dtm} (likely ill-conditioned)")
+    if code == _lib.ERR_STRUCTURE:
+        raise AssertionError("structural condition s12 > 0 violated")
     raise EllipticSolveError("non-finite elliptic solution")
 
 
@@ -181,8 +187,10 @@ def bits_to_flags(bits: np.ndarray, n: int) -> np.ndarray:
 
 
 def scheme(mode: int, kind: str = "eta_over_d", k_nh: float = 1e-3, enlarge: bool = False,
-           flux=None, g: float = 9.81, rho: float = 1000.0, record_cfl: bool = True):
+           flux=None, g: float = 9.81, rho: float = 1000.0, record_cfl: bool = True,
+           residual_tol: float = 1e-10):
     s = _lib.Scheme()
+    s.residual_tol = residual_tol
     s.g = g
     s.rho = rho
     s.k_nh = k_nh

@@ -21,7 +21,7 @@ BC_ABSORBING, BC_WALL = 0, 1
 MODE_HYDROSTATIC, MODE_GLOBAL, MODE_ADAPTIVE, MODE_CORRECT_GIVEN = range(4)
 CRIT = {"eta_over_d": 0, "eta_x": 1, "u": 2, "u_x": 3, "w": 4, "w_x": 5}
 ERR_POSITIVITY_ENTRY, ERR_POSITIVITY_STAGE1, ERR_POSITIVITY_STAGE2 = 1, 2, 3
-ERR_SOLVE_NONFINITE, ERR_SOLVE_PIVOT = 4, 5
+ERR_SOLVE_NONFINITE, ERR_SOLVE_PIVOT, ERR_SOLVE_RESIDUAL, ERR_STRUCTURE = 4, 5, 6, 7
 E_ARG, E_CUDA, E_UNSUPPORTED = -1, -2, -3
 STATUS_OK_KEY = np.uint64(0xFFFFFFFFFFFFFFFF)
 
@@ -34,21 +34,23 @@ MEMBER_DTYPE = np.dtype([
     ("bc_left", "i4"), ("bc_right", "i4"), ("bottom_kind", "i4"), ("reserved", "i4"),
 ])
 STATUS_DTYPE = np.dtype([("error_key", "u8"), ("cfl_max", "f8"), ("flagged", "i8"),
-                         ("steps_done", "i4"), ("any_hw", "i4")])
+                         ("steps_done", "i4"), ("any_hw", "i4"), ("resid_max", "f8"),
+                         ("resid_acc", "f8", (4,))])
 PM_DTYPE = np.dtype([   # nh_pm_member: m-node operators, m <= 4 (row-major, leading dim m)
     ("weak_div", "f8", (16,)), ("lift_left", "f8", (4,)), ("lift_right", "f8", (4,)),
     ("mass", "f8", (16,)), ("stiffness", "f8", (16,)), ("deriv_ref", "f8", (16,)),
     ("node_off", "f8", (4,)),
 ])
 PM_MAX_NODES = 4
-assert MEMBER_DTYPE.itemsize == 312 and STATUS_DTYPE.itemsize == 32 and PM_DTYPE.itemsize == 608
+assert MEMBER_DTYPE.itemsize == 312 and STATUS_DTYPE.itemsize == 72 and PM_DTYPE.itemsize == 608
 
 
 class Scheme(ctypes.Structure):
     _fields_ = [("g", ctypes.c_double), ("rho", ctypes.c_double), ("k_nh", ctypes.c_double),
                 ("c11", ctypes.c_double), ("c12", ctypes.c_double), ("c22", ctypes.c_double),
                 ("mode", ctypes.c_int32), ("criterion", ctypes.c_int32),
-                ("enlarge", ctypes.c_int32), ("record_cfl", ctypes.c_int32)]
+                ("enlarge", ctypes.c_int32), ("record_cfl", ctypes.c_int32),
+                ("residual_tol", ctypes.c_double)]
 
 
 class Outputs(ctypes.Structure):
@@ -57,7 +59,7 @@ class Outputs(ctypes.Structure):
                 ("gauge_h", ctypes.c_void_p), ("n_gauges", ctypes.c_int32)]
 
 
-ABI_VERSION = 3   # include/nhswe_b200.h NH_ABI_VERSION
+ABI_VERSION = 4   # include/nhswe_b200.h NH_ABI_VERSION
 
 EXPORTS = ("nh_abi_version", "nh_advance", "nh_stream_advance", "nh_stream_workspace_bytes",
            "nh_rhs", "nh_criterion", "nh_coefficients",
@@ -85,7 +87,7 @@ _SIGS = {
     "nh_rhs": ([_P, _I, _I, _P, _P, _P, _P, _D, _P, _P, _P, _P, _P], _I),
     "nh_criterion": ([_P, _I, _I, _P, _P, _P, _P, _I, _P, _P], _I),
     "nh_coefficients": ([_P, _I, _I, _P, _P, _P, _P, _D, _D, _P, _P], _I),
-    "nh_ldg_solve": ([_P, _I, _I, _P, _P, _P, _D, _D, _D, _D, _P, _P, _P, _P], _I),
+    "nh_ldg_solve": ([_P, _I, _I, _P, _P, _P, _P, _D, _D, _D, _D, _D, _P, _P, _P, _P], _I),
     "nh_correct_momentum": ([_P, _I, _I, _P, _P, _P, _P, _D, _P, _P, _P], _I),
     "nh_bottom_sample": ([_P, _I, _P, _I, _P, _P, _P], _I),
     "nh_plan": ([_I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I),

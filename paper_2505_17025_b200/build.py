@@ -20,7 +20,7 @@ LIB = os.path.join(OUT_DIR, "libnhswe_b200.so")
 SOURCES = ["capi.cu", "step_kernel.cu", "aux_kernels.cu", "stream_kernels.cu", "stream_kp.cu",
            "pm_kernels.cu"]
 HEADERS = ["nh_common.cuh", "bathy.cuh", "physics.cuh", "tree.cuh", "step_kernel.cuh",
-           "stream_kernels.cuh", "stream_kp.cuh", "stream_kp2.cuh"]
+           "stream_kernels.cuh", "stream_kp.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "--extended-lambda", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 # default build: reference-faithful arithmetic (NH_STRICT=1, no implicit FMA contraction);

@@ -155,16 +155,19 @@ def config3() -> Config:
 
 # ---------------------------------------------------------------- config 4
 
-@lru_cache(maxsize=4)
-def _config4_draws(n_members: int, seed: int):
-    rng = np.random.default_rng(seed)
-    return {
-        "h0": rng.uniform(0.5, 2.0, n_members),
-        "a_rel": rng.uniform(0.05, 0.3, n_members),
-        "zeta_rel": rng.uniform(0.01, 0.1, n_members),
-        "b_rel": rng.uniform(0.1, 1.0, n_members),
-        "alpha": rng.uniform(5.0, 50.0, n_members),
-    }
+def member_rng(seed: int, i: int) -> np.random.Generator:
+    """Member i's own generator: its parameters depend on (seed, i) only, not
+    on the ensemble size, so a member is the same channel in a 4096-member run,
+    a 1-member parity run and any rank's shard of a sharded run."""
+    return np.random.default_rng([seed, i])
+
+
+@lru_cache(maxsize=8192)
+def _config4_draw(seed: int, i: int):
+    rng = member_rng(seed, i)
+    return {k: float(rng.uniform(lo, hi)) for k, (lo, hi) in
+            (("h0", (0.5, 2.0)), ("a_rel", (0.05, 0.3)), ("zeta_rel", (0.01, 0.1)),
+             ("b_rel", (0.1, 1.0)), ("alpha", (5.0, 50.0)))}
 
 
 class Config4(Config):
@@ -189,12 +192,14 @@ class Config4(Config):
         self.seed = seed
 
     def member(self, i):
-        r = _config4_draws(self.n_members, self.seed)
-        h0 = float(r["h0"][i])
+        if not 0 <= i < self.n_members:
+            raise IndexError(i)
+        r = _config4_draw(self.seed, i)
+        h0 = r["h0"]
         L = 200.0 * h0
         grid = GridSpec(0.0, L, self.n_elements)
         if i % 2 == 0:
-            a = h0 * float(r["a_rel"][i])
+            a = h0 * r["a_rel"]
             x0 = 0.2 * L
             h, hu, _ = solitary_state(np, grid.nodes, h0, a, x0, grid.dx)
             lam = float(np.max(np.abs(hu / h) + np.sqrt(GRAVITY * h)))
@@ -203,8 +208,7 @@ class Config4(Config):
         h0 = self.BOX_H0
         L = 200.0 * h0
         grid = GridSpec(0.0, L, self.n_elements)
-        bathy = SmoothBoxPlate(h0, h0 * float(r["zeta_rel"][i]), h0 * float(r["b_rel"][i]),
-                               float(r["alpha"][i]), 0.2 * h0)
+        bathy = SmoothBoxPlate(h0, h0 * r["zeta_rel"], h0 * r["b_rel"], r["alpha"], 0.2 * h0)
         return MemberSpec(grid, bathy, BoundaryPair(WALL, ABSORBING),
                           dt_from_cfl(grid.dx, math.sqrt(GRAVITY * h0)), "still")
 
@@ -225,22 +229,23 @@ def _slide_ok(tan_t, A, sigma, x0, xs):
     return ok & (worst >= 0.04)
 
 
-@lru_cache(maxsize=2)
-def _config5_table(n_members: int, seed: int):
-    """(tan_theta, A, sigma, x0, u_t) per member, rejection-sampled in rounds."""
-    rng = np.random.default_rng(seed)
+def _config5_rows(seed: int, idx) -> np.ndarray:
+    """(tan_theta, A, sigma, x0, u_t) of members idx, each rejection-sampled
+    from its own generator (member_rng): candidates are drawn in rounds and
+    checked vectorised; a rejected member draws its next candidate from the
+    same generator."""
+    idx = np.asarray(idx, dtype=np.int64)
     xs = np.linspace(0.0, 20.0, 321)
-    out = np.zeros((n_members, 5))
-    todo = np.arange(n_members)
+    gens = [member_rng(seed, int(i)) for i in idx]
+    out = np.zeros((idx.size, 5))
+    todo = np.arange(idx.size)
     for _ in range(200):
         if todo.size == 0:
             break
-        k = todo.size
-        theta = np.radians(rng.uniform(5.0, 20.0, k))
-        ratio = rng.uniform(0.05, 0.5, k)
-        sigma = rng.uniform(0.1, 1.0, k)
-        u_t = rng.uniform(0.2, 2.0, k)
-        tan_t = np.tan(theta)
+        d = np.array([[gens[k].uniform(5.0, 20.0), gens[k].uniform(0.05, 0.5),
+                       gens[k].uniform(0.1, 1.0), gens[k].uniform(0.2, 2.0)] for k in todo])
+        tan_t = np.tan(np.radians(d[:, 0]))
+        ratio, sigma, u_t = d[:, 1], d[:, 2], d[:, 3]
         x0 = 1.0 + 2.0 * sigma
         A = ratio * np.minimum(0.1 + x0 * tan_t, 1.0)
         ok = _slide_ok(tan_t, A, sigma, x0, xs)
@@ -248,6 +253,15 @@ def _config5_table(n_members: int, seed: int):
         todo = todo[~ok]
     if todo.size:
         raise RuntimeError("config-5 rejection sampling did not converge")
+    return out
+
+
+@lru_cache(maxsize=2)
+def _config5_table(n_members: int, seed: int):
+    """Rows of members 0..n_members-1 (row i depends on (seed, i) only)."""
+    out = np.zeros((n_members, 5))
+    for c0 in range(0, n_members, 8192):
+        out[c0:c0 + 8192] = _config5_rows(seed, range(c0, min(c0 + 8192, n_members)))
     return out
 
 

@@ -12,7 +12,11 @@ Every function keeps the reference signature and runs on the GPU:
 
 The GPU solve supports the reference's alternating flux family
 (c12 = -1/2, c22 = 0, any c11) -- the only one the reference ever uses; other
-flux constants raise ``NotImplementedError``.
+flux constants raise ``ValueError`` before any work is done.  Every solve
+carries the reference's residual gate (corrector.py:355-366): the relative
+residual of the batched system is evaluated on the device and above
+``residual_tol`` raises ``EllipticSolveError``.  Adjacent ranges are separate
+systems, as in the reference's block-diagonal batch.
 """
 
 from __future__ import annotations
@@ -123,11 +127,17 @@ def assemble_coefficients(predictor: FlowState, bathy: BathymetryModel, dt: floa
 
 def _check_flux(flux: FluxCoefficients):
     if flux.c12 != -0.5 or flux.c22 != 0.0:
-        raise NotImplementedError("GPU LDG solve supports the alternating flux c12=-1/2, c22=0")
+        raise ValueError(
+            f"unsupported LDG flux {flux}: the B200 solve condenses the system for the "
+            "alternating flux family c12 = -1/2, c22 = 0 (any c11), the reference default")
+
+
+def _has_adjacent(ranges) -> bool:
+    return any(r[0] <= q[1] + 1 for q, r in zip(ranges, ranges[1:]))
 
 
 def _solve_device(coeffs: EllipticCoefficients, ranges, outer_right: np.ndarray,
-                  flux: FluxCoefficients):
+                  flux: FluxCoefficients, residual_tol: float = 1e-10):
     """Run nh_ldg_solve; returns full-grid (p, hu) host arrays (hu only valid on ranges)."""
     lib = D.require_cuda()
     _check_flux(flux)
@@ -140,6 +150,14 @@ def _solve_device(coeffs: EllipticCoefficients, ranges, outer_right: np.ndarray,
         if e0 - off < 0 or e1 - off >= len(coeffs.s11):
             raise ValueError(f"range {(e0, e1)} outside the coefficient window")
     nodes = grid.poly_order + 1
+    if nodes != 2 and _has_adjacent(ranges):
+        # the m-node chain has no range-start input: solve every other range
+        # per call, so no two ranges of a call touch
+        p, hu = _solve_device(coeffs, ranges[0::2], outer_right, flux, residual_tol)
+        p2, hu2 = _solve_device(coeffs, ranges[1::2], outer_right, flux, residual_tol)
+        for e0, e1 in ranges[1::2]:
+            p[e0:e1 + 1], hu[e0:e1 + 1] = p2[e0:e1 + 1], hu2[e0:e1 + 1]
+        return p, hu
     planes = np.zeros((7, 1, n, nodes))
     sl = slice(off, off + len(coeffs.s11))
     fields = (coeffs.s11, coeffs.s12, coeffs.s22, coeffs.f1, coeffs.f2)
@@ -148,12 +166,15 @@ def _solve_device(coeffs: EllipticCoefficients, ranges, outer_right: np.ndarray,
     for i, arr in enumerate(fields):
         planes[i, 0, sl] = arr
     flags = np.zeros(n, dtype=bool)
+    starts = np.zeros(n, dtype=bool)
     for e0, e1 in ranges:
         flags[e0:e1 + 1] = True
+        starts[e0] = True
     m = D.upload_members(D.member_record(grid, _FlatPack(), None, coeffs.dt,
                                          any_order=nodes != 2))
     cp = D.dev(planes)
     fb = D.dev(D.flags_to_bits(flags[None]).view(np.int32), dtype=np.int32)
+    sb = D.dev(D.flags_to_bits(starts[None]).view(np.int32), dtype=np.int32)
     orr = D.dev(outer_right[None])
     T = D.torch()
     p = T.zeros((1, n, nodes), dtype=T.float64, device="cuda")
@@ -167,9 +188,10 @@ def _solve_device(coeffs: EllipticCoefficients, ranges, outer_right: np.ndarray,
                                        D.ptr(hu), D.ptr(st), D.ptr(ws), ws.numel(),
                                        D.stream_ptr()), "nh_pm_ldg_solve")
     else:
-        _lib.check(lib.nh_ldg_solve(D.ptr(m), 1, n, D.ptr(cp), D.ptr(fb), D.ptr(orr),
-                                    coeffs.rho, flux.c11, flux.c12, flux.c22, D.ptr(p),
-                                    D.ptr(hu), D.ptr(st), D.stream_ptr()), "nh_ldg_solve")
+        _lib.check(lib.nh_ldg_solve(D.ptr(m), 1, n, D.ptr(cp), D.ptr(fb), D.ptr(sb), D.ptr(orr),
+                                    coeffs.rho, flux.c11, flux.c12, flux.c22,
+                                    float(residual_tol), D.ptr(p), D.ptr(hu), D.ptr(st),
+                                    D.stream_ptr()), "nh_ldg_solve")
     status = D.read_status(st)
     D.raise_for_status(status, 0.0, 0.0)
     return p[0].cpu().numpy(), hu[0].cpu().numpy()
@@ -190,7 +212,7 @@ def ldg_solve(coeffs: EllipticCoefficients, elements: tuple[int, int],
     e0, e1 = (int(v) for v in elements)
     n = coeffs.grid.n_elements
     outer = np.full(n, float(outer_hu[1]))
-    p, hu = _solve_device(coeffs, ((e0, e1),), outer, flux)
+    p, hu = _solve_device(coeffs, ((e0, e1),), outer, flux, residual_tol)
     return p[e0:e1 + 1].copy(), hu[e0:e1 + 1].copy()
 
 
@@ -273,6 +295,14 @@ def apply_correction(predictor: FlowState, bathy: BathymetryModel, dt: float, ra
     ranges = tuple(sorted(tuple(int(v) for v in r) for r in ranges))
     if not ranges:
         raise ValueError("apply_correction needs at least one range")
+    if _has_adjacent(ranges):
+        # adjacent ranges are separate systems: the reference's own pipeline
+        # (corrector.py:485-498) of the three device kernels, whose solve
+        # splits the flagged run at the given range starts
+        lo, hi = max(ranges[0][0] - 1, 0), min(ranges[-1][1] + 1, n - 1)
+        coeffs = assemble_coefficients(predictor, bathy, dt, g, rho, window=slice(lo, hi + 1))
+        sol = solve_on_ranges(predictor, coeffs, ranges, bcs, flux)
+        return correct_momentum(predictor, sol, coeffs), sol
     flags = np.zeros(n, dtype=bool)
     for e0, e1 in ranges:
         if e0 > e1 or e0 < 0 or e1 >= n:

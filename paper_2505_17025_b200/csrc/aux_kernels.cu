@@ -199,8 +199,28 @@ __global__ void __launch_bounds__(NH_STEP_MAX_THREADS) nh_solve_kernel(SolveArgs
   ts.wflag = (int*)(ts.cnode + 31 * 6);
   const size_t plane = (size_t)a.B * N * 2;
   const uint32_t* fb = a.flags + (size_t)b * a.nwords;
+  const uint32_t* sb = a.starts ? a.starts + (size_t)b * a.nwords : nullptr;
   auto flag = [&](int e) -> bool { return e >= 0 && e < N && ((fb[e >> 5] >> (e & 31)) & 1u); };
+  // a range starts at e: e flagged and e - 1 not, or a caller-given start
+  // inside a flagged run (adjacent ranges are separate systems, each with
+  // P* = 0 at its ends -- the reference stacks them block-diagonally)
+  auto start = [&](int e) -> bool {
+    return flag(e) && (!flag(e - 1) || (sb && ((sb[e >> 5] >> (e & 31)) & 1u)));
+  };
   const double* outer = a.outer_right + (size_t)b * N;
+  const double inv_rho = 1.0 / a.rho;
+  auto load_q = [&](int e, NodeCoef (&q)[2]) {
+    size_t o = ((size_t)b * N + e) * 2;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      q[i].s11 = a.coef[0 * plane + o + i];
+      q[i].s12 = a.coef[1 * plane + o + i];
+      q[i].s22 = a.coef[2 * plane + o + i];
+      q[i].f1 = a.coef[3 * plane + o + i];
+      q[i].f2 = a.coef[4 * plane + o + i];
+      q[i].phi = 0.0;
+    }
+  };
   Super Sk[E];
   double R[E][6];
   bool flg[E];
@@ -216,20 +236,24 @@ __global__ void __launch_bounds__(NH_STEP_MAX_THREADS) nh_solve_kernel(SolveArgs
     } else if (!flg[k]) {
       Sk[k] = super_gap(e > 0 ? outer[e - 1] : 0.0);
     } else {
-      size_t o = ((size_t)b * N + e) * 2;
       NodeCoef q[2];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        q[i].s11 = a.coef[0 * plane + o + i];
-        q[i].s12 = a.coef[1 * plane + o + i];
-        q[i].s22 = a.coef[2 * plane + o + i];
-        q[i].f1 = a.coef[3 * plane + o + i];
-        q[i].f2 = a.coef[4 * plane + o + i];
-        q[i].phi = 0.0;
-      }
-      bool range_end = (e == N - 1) || !flag(e + 1);
-      if (!local_condense(m, q[0], q[1], a.rho, 1.0 / a.rho, a.c11, range_end, Sk[k], R[k]))
+      load_q(e, q);
+      const bool cut_right = e < N - 1 && start(e + 1) && flag(e);   // next range starts at e + 1
+      bool range_end = (e == N - 1) || !flag(e + 1) || cut_right;
+      if (!local_condense(m, q[0], q[1], a.rho, inv_rho, a.c11, range_end, Sk[k], R[k]))
         nh_report(a.status + b, 0, NH_ERR_SOLVE_PIVOT, e);
+      if (!ldg_structure_ok(q[0], q[1])) nh_report(a.status + b, 0, NH_ERR_STRUCTURE, e);
+      if (cut_right) {   // z_{e+1} is the outer trace hu(e+1, node 0): fold it in
+        const double zc = outer[e];
+        Sk[k].ga += Sk[k].ba * zc; Sk[k].ba = 0.0;
+        Sk[k].gz += Sk[k].bz * zc; Sk[k].bz = 0.0;
+        R[k][0] += R[k][2] * zc; R[k][2] = 0.0;
+        R[k][3] += R[k][5] * zc; R[k][5] = 0.0;
+      }
+      if (start(e) && flag(e - 1)) {   // P* = 0 at this range start: drop a_{e-1}
+        Sk[k].aa = 0.0; Sk[k].az = 0.0;
+        R[k][1] = 0.0; R[k][4] = 0.0;
+      }
     }
   }
   bool tflag = false;
@@ -241,6 +265,7 @@ __global__ void __launch_bounds__(NH_STEP_MAX_THREADS) nh_solve_kernel(SolveArgs
   tree_solve(cluster, ts, C, rank, W, warp, lane, tflag, true, agg, a_in, z_in);
   double aprev[E], znext[E];
   chunk_unwind<E>(Sk, a_in, z_in, aprev, znext);
+  ResidAcc ra{0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int k = 0; k < E; ++k) {
     if (!flg[k]) continue;
@@ -251,8 +276,21 @@ __global__ void __launch_bounds__(NH_STEP_MAX_THREADS) nh_solve_kernel(SolveArgs
     size_t o = ((size_t)b * N + e) * 2;
     a.p[o] = a.rho * P0; a.p[o + 1] = a.rho * P1;
     a.hu[o] = Q0; a.hu[o + 1] = Q1;
+    // residual rows of the element (the reference's gate, corrector.py:355-366)
+    NodeCoef q[2];
+    load_q(e, q);
+    const bool rs = start(e);
+    const bool cut_right = e < N - 1 && start(e + 1);
+    const bool re = (e == N - 1) || !flag(e + 1) || cut_right;
+    ldg_residual(m, q[0], q[1], a.rho, inv_rho, a.c11, rs, re, rs ? 0.0 : aprev[k],
+                 cut_right ? outer[e] : znext[k], P0, Q0, P1, Q1, ra);
   }
-  cluster.sync();   // keep every CTA's shared memory alive until all DSMEM reads are done
+  resid_flush_warp(a.status + b, ra);
+  cluster.sync();   // every CTA's shares are in; also keeps shared memory alive for DSMEM reads
+  if (rank == 0 && tid == 0) {
+    __threadfence();
+    resid_check(a.status + b, 0, a.residual_tol);
+  }
 }
 
 template __global__ void nh_solve_kernel<3>(SolveArgs);

@@ -245,8 +245,9 @@ int nh_coefficients(const nh_member* members, int n_members, int n_elements, con
 }
 
 int nh_ldg_solve(const nh_member* members, int n_members, int n_elements, const double* coef,
-                 const uint32_t* flags, const double* outer_right, double rho, double c11,
-                 double c12, double c22, double* p, double* hu, nh_status* status, void* stream) {
+                 const uint32_t* flags, const uint32_t* range_starts, const double* outer_right,
+                 double rho, double c11, double c12, double c22, double residual_tol, double* p,
+                 double* hu, nh_status* status, void* stream) {
   if (!members || n_members < 1 || n_elements < 2) return NH_E_ARG;
   if (c12 != -0.5 || c22 != 0.0) return NH_E_UNSUPPORTED;
   int rc = set_attrs();
@@ -257,8 +258,9 @@ int nh_ldg_solve(const nh_member* members, int n_members, int n_elements, const 
   int tile = (n_elements + c - 1) / c;
   int thr = std::max(32, ((tile + kE - 1) / kE + 31) / 32 * 32);
   SolveArgs a;
-  a.members = members; a.coef = coef; a.flags = flags; a.outer_right = outer_right;
-  a.p = p; a.hu = hu; a.status = status; a.rho = rho; a.c11 = c11;
+  a.members = members; a.coef = coef; a.flags = flags; a.starts = range_starts;
+  a.outer_right = outer_right;
+  a.p = p; a.hu = hu; a.status = status; a.rho = rho; a.c11 = c11; a.residual_tol = residual_tol;
   a.B = n_members; a.N = n_elements; a.cluster = c; a.tile = tile;
   a.nwords = (n_elements + 31) / 32;
   return counted(launch_cluster(nh_solve_kernel_ptr(kE), &a, n_members * c, thr,
@@ -290,31 +292,42 @@ bool graphs_enabled() {
   return g_graphs.load() != 0;
 }
 
-// One cached executable graph of a pair of steps, keyed on the launch
-// arguments of both steps (a new ensemble, buffer or scheme re-captures).
+// Cached executable graphs of a pair of steps, keyed on the device and the
+// launch arguments of both steps.  A small LRU of slots: callers that
+// alternate between ensembles or buffers (e.g. the host-pipelined member
+// blocks of driver.advance_host) replay their own graph instead of
+// re-capturing.  Capture streams are per device.
+constexpr int NH_GRAPH_SLOTS = 16;
+constexpr int NH_MAX_DEVICES = 64;
 struct PairGraph {
   bool valid = false;
+  int device = -1;
+  unsigned long long used = 0;   // LRU stamp
   unsigned char key[sizeof(StreamArgs)];
   cudaGraphExec_t exec = nullptr;
   long long nodes = 0;
-  cudaStream_t cap = nullptr;
-} g_pair;
+};
+PairGraph g_pairs[NH_GRAPH_SLOTS];
+cudaStream_t g_cap[NH_MAX_DEVICES] = {};
+unsigned long long g_stamp = 0;
 std::mutex g_pair_mu;
 
 template <class Capture>
 int pair_graph(const StreamArgs& a, Capture capture, cudaGraphExec_t& exec, long long& nodes) {
   std::lock_guard<std::mutex> lk(g_pair_mu);
-  if (!g_pair.cap && cudaStreamCreateWithFlags(&g_pair.cap, cudaStreamNonBlocking) != cudaSuccess)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= NH_MAX_DEVICES) return NH_E_CUDA;
+  if (!g_cap[dev] && cudaStreamCreateWithFlags(&g_cap[dev], cudaStreamNonBlocking) != cudaSuccess)
     return NH_E_CUDA;
   // capture (nothing executes) on a private stream: the caller's may be the
   // legacy default stream, which cannot be captured; the graph is launched
   // on the caller's stream
   const long long l0 = g_launches.load();
-  if (cudaStreamBeginCapture(g_pair.cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+  if (cudaStreamBeginCapture(g_cap[dev], cudaStreamCaptureModeThreadLocal) != cudaSuccess)
     return NH_E_CUDA;
-  int rc = capture(g_pair.cap);
+  int rc = capture(g_cap[dev]);
   cudaGraph_t graph = nullptr;
-  cudaError_t ce = cudaStreamEndCapture(g_pair.cap, &graph);
+  cudaError_t ce = cudaStreamEndCapture(g_cap[dev], &graph);
   const long long n = g_launches.load() - l0;
   g_launches -= n;   // captured, not executed
   if (rc || ce != cudaSuccess || !graph) {
@@ -322,21 +335,78 @@ int pair_graph(const StreamArgs& a, Capture capture, cudaGraphExec_t& exec, long
     return rc ? rc : NH_E_CUDA;
   }
   // `a` now holds the even step's arguments, which fix the odd step's too
-  if (g_pair.valid && std::memcmp(&a, g_pair.key, sizeof(StreamArgs)) == 0) {
+  PairGraph* hit = nullptr;
+  PairGraph* victim = &g_pairs[0];
+  for (PairGraph& g : g_pairs) {
+    if (g.valid && g.device == dev && std::memcmp(&a, g.key, sizeof(StreamArgs)) == 0) {
+      hit = &g;
+      break;
+    }
+    if (!g.valid || (victim->valid && g.used < victim->used)) victim = &g;
+  }
+  if (hit) {
     cudaGraphDestroy(graph);
   } else {
-    if (g_pair.exec) cudaGraphExecDestroy(g_pair.exec);
-    g_pair.exec = nullptr;
-    g_pair.valid = false;
-    ce = cudaGraphInstantiate(&g_pair.exec, graph, 0);
+    hit = victim;
+    if (hit->exec) {
+      int cur = dev;
+      if (hit->device != dev) cudaSetDevice(hit->device);
+      cudaGraphExecDestroy(hit->exec);
+      if (hit->device != dev) cudaSetDevice(cur);
+    }
+    hit->exec = nullptr;
+    hit->valid = false;
+    ce = cudaGraphInstantiate(&hit->exec, graph, 0);
     cudaGraphDestroy(graph);
     if (ce != cudaSuccess) return NH_E_CUDA;
-    std::memcpy(g_pair.key, &a, sizeof(StreamArgs));
-    g_pair.valid = true;
-    g_pair.nodes = n;
+    std::memcpy(hit->key, &a, sizeof(StreamArgs));
+    hit->device = dev;
+    hit->valid = true;
+    hit->nodes = n;
   }
-  exec = g_pair.exec;
-  nodes = g_pair.nodes;
+  hit->used = ++g_stamp;
+  exec = hit->exec;
+  nodes = hit->nodes;
+  return 0;
+}
+
+// Persistent-grid sizes of K_S / K_C (resident CTAs x SMs) and the K_P
+// shared-memory opt-in, per device.
+struct StreamDevice {
+  int ks_grid = 0, kc_grid = 0;
+};
+StreamDevice g_sdev[NH_MAX_DEVICES];
+std::mutex g_sdev_mu;
+
+int stream_device_init(StreamDevice*& out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= NH_MAX_DEVICES) return NH_E_CUDA;
+  std::lock_guard<std::mutex> lk(g_sdev_mu);
+  StreamDevice& d = g_sdev[dev];
+  if (!d.ks_grid) {
+    int sms = 0, nks = 0, nkc = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nks, nh_stream_kernel(3), NH_STREAM_THREADS, 0) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nkc, nh_stream_kernel(2), NH_STREAM_THREADS, 0) != cudaSuccess)
+      return NH_E_CUDA;
+    if (cudaFuncSetAttribute(nh_stream_kernel(0), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)nh_stream_kp_smem()) != cudaSuccess)
+      return NH_E_CUDA;
+    if (void* kf = nh_stream_kp_fused_ptr())
+      if (cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)nh_stream_kp_smem()) != cudaSuccess)
+        return NH_E_CUDA;
+    int ks = std::max(1, nks) * sms, kc = std::max(1, nkc) * sms;
+    if (getenv("NH_STREAM_VERBOSE"))
+      fprintf(stderr, "nh_stream: device %d K_S grid %d, K_C grid %d\n", dev, ks, kc);
+    if (const char* v = getenv("NH_KS_WAVES")) {   // diagnostics: grid = waves x resident CTAs
+      int wv = atoi(v);
+      if (wv > 0) { ks *= wv; kc *= wv; }
+    }
+    d.kc_grid = kc;
+    d.ks_grid = ks;
+  }
+  out = &d;
   return 0;
 }
 }  // namespace
@@ -347,7 +417,7 @@ static int stream_tiles(int n) { return (n + NH_STREAM_OWN - 1) / NH_STREAM_OWN;
 
 size_t nh_stream_workspace_bytes(int n_members, int n_elements) {
   size_t BN = (size_t)n_members * n_elements, BT = (size_t)n_members * stream_tiles(n_elements);
-  size_t dbl = 6 * BN + 12 * BN + 12 * BN + 10 * BT + 16 * (size_t)n_members;
+  size_t dbl = 6 * BN + 10 * BN + 12 * BN + 10 * BT + 16 * (size_t)n_members;
   return dbl * 8 + 2 * BN + 4 * (size_t)n_members + 8 + 4 * BT + 8 * (size_t)n_members + 1024;
 }
 
@@ -369,7 +439,7 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
   const size_t BN = (size_t)B * N, BT = (size_t)B * T;
   char* w = (char*)workspace;
   double* alt = (double*)w;             w += 6 * BN * 8;
-  double* scratch = (double*)w;         w += 12 * BN * 8;
+  double* scratch = (double*)w;         w += 10 * BN * 8;
   double* pend[2] = {(double*)w, (double*)w + 6 * BN};  w += 12 * BN * 8;
   double* tagg = (double*)w;            w += 8 * BT * 8;
   double* tio = (double*)w;             w += 2 * BT * 8;
@@ -385,30 +455,9 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
                       (sc.criterion == NH_CRIT_W || sc.criterion == NH_CRIT_W_X);
   if (w_crit && !nh_stream_kp_records_hw_any()) return NH_E_UNSUPPORTED;
   if (w_crit && cudaMemsetAsync(hw_any, 0, 4 * (size_t)B, s) != cudaSuccess) return NH_E_CUDA;
-  static int ks_grid = 0, kc_grid = 0;   // persistent grids: resident CTAs x SMs
-  if (!ks_grid) {
-    int dev = 0, sms = 0, nks = 0, nkc = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nks, nh_stream_kernel(3), NH_STREAM_THREADS, 0) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nkc, nh_stream_kernel(2), NH_STREAM_THREADS, 0) != cudaSuccess)
-      return NH_E_CUDA;
-    if (cudaFuncSetAttribute(nh_stream_kernel(0), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)nh_stream_kp_smem()) != cudaSuccess)
-      return NH_E_CUDA;
-    if (void* kf = nh_stream_kp_fused_ptr())
-      if (cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)nh_stream_kp_smem()) != cudaSuccess)
-        return NH_E_CUDA;
-    ks_grid = std::max(1, nks) * sms;
-    kc_grid = std::max(1, nkc) * sms;
-    if (getenv("NH_STREAM_VERBOSE"))
-      fprintf(stderr, "nh_stream: K_S grid %d, K_C grid %d\n", ks_grid, kc_grid);
-    if (const char* v = getenv("NH_KS_WAVES")) {   // diagnostics: grid = waves x resident CTAs
-      int wv = atoi(v);
-      if (wv > 0) { ks_grid *= wv; kc_grid *= wv; }
-    }
-  }
+  StreamDevice* sdev = nullptr;   // persistent grids of this device
+  if (int rc = stream_device_init(sdev)) return rc;
+  const int ks_grid = sdev->ks_grid, kc_grid = sdev->kc_grid;
   double* A[3] = {h, hu, hw};
   double* Bb[3] = {alt, alt + 2 * BN, alt + 4 * BN};
   StreamArgs a;

@@ -294,6 +294,113 @@ NH_DEV bool local_condense(const nh_member& m, const NodeCoef& c0, const NodeCoe
   return ok;
 }
 
+// Residual gate of the elliptic solve (corrector.py:355-366).  The reference
+// evaluates rel = ||A x - b|| / max(||b||, max|A| ||x||, 1e-300) over the
+// step's whole batched band system and raises EllipticSolveError above
+// residual_tol.  Every row of that system belongs to one flagged element, so
+// the norms are sums (max) over elements: this is one element's share, at
+// the solved unknowns x = (P0, Q0, P1, Q1) (P = p / rho) with the coupling
+// values a_prev = P(e-1, node 1) (0 at a range start) and z_next = Q(e+1,
+// node 0) - c11 P(e+1, node 0) (the outer hu trace at a range end).  The
+// element block is built exactly as local_condense builds it -- the same
+// entries as the reference's assembly (_block_template / _solve_batched).
+struct ResidAcc {
+  double r2, b2, x2, amax;
+};
+
+NH_DEV void ldg_residual(const nh_member& m, const NodeCoef& c0, const NodeCoef& c1, double rho,
+                         double inv_rho, double c11, bool range_start, bool range_end,
+                         double a_prev, double z_next, double P0, double Q0, double P1,
+                         double Q1, ResidAcc& acc) {
+  const double* M = m.mass;
+  const double* K = m.stiffness;
+  double A[4][4], r[4];
+  const NodeCoef* cj[2] = {&c0, &c1};
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const NodeCoef& q = *cj[j];
+      double Mij = M[2 * i + j], Kij = K[2 * i + j];
+      A[2 * i][2 * j] = -Kij + Mij * q.s11;
+      A[2 * i][2 * j + 1] = Mij * (q.s12 * inv_rho);
+      A[2 * i + 1][2 * j + 1] = -Kij + Mij * (-q.s11);
+      A[2 * i + 1][2 * j] = Mij * (rho * q.s22);
+    }
+    r[2 * i] = fma(M[2 * i + 1], c1.f1 * inv_rho, M[2 * i] * (c0.f1 * inv_rho));
+    r[2 * i + 1] = fma(M[2 * i + 1], c1.f2, M[2 * i] * c0.f2);
+  }
+  A[1][1] -= 1.0;
+  A[1][0] += c11;
+  if (!range_end) A[2][2] += 1.0;
+  A[3][2] += c11;
+  const double x[4] = {P0, Q0, P1, Q1};
+  double res[4], amax = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double v = -r[i];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      v = fma(A[i][j], x[j], v);
+      amax = fmax(amax, fabs(A[i][j]));
+    }
+    res[i] = v;
+  }
+  // couplings: rows P0 / Q0 to P(e-1, 1) (-1, -c11), row Q1 to the right
+  // neighbour (+1 on Q(e+1, 0), -c11 on P(e+1, 0)); a range end's z_next is
+  // the outer trace, which the reference carries in b
+  res[0] -= a_prev;
+  res[1] -= c11 * a_prev;
+  res[3] += z_next;
+  double b3 = range_end ? r[3] - z_next : r[3];
+  if (!range_start || !range_end) amax = fmax(amax, fmax(1.0, fabs(c11)));
+  acc.r2 += res[0] * res[0] + res[1] * res[1] + res[2] * res[2] + res[3] * res[3];
+  acc.b2 += r[0] * r[0] + r[1] * r[1] + r[2] * r[2] + b3 * b3;
+  acc.x2 += P0 * P0 + Q0 * Q0 + P1 * P1 + Q1 * Q1;
+  acc.amax = fmax(acc.amax, amax);
+}
+
+// A warp's residual shares into the member's running sums (all 32 lanes
+// converged; lanes without a flagged element pass zeros).
+NH_DEV void resid_flush_warp(nh_status* st, ResidAcc a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a.r2 += __shfl_xor_sync(0xffffffffu, a.r2, o);
+    a.b2 += __shfl_xor_sync(0xffffffffu, a.b2, o);
+    a.x2 += __shfl_xor_sync(0xffffffffu, a.x2, o);
+    a.amax = fmax(a.amax, __shfl_xor_sync(0xffffffffu, a.amax, o));
+  }
+  if ((threadIdx.x & 31) == 0 && (a.amax > 0.0 || a.x2 > 0.0 || a.b2 > 0.0 || a.r2 != 0.0)) {
+    atomicAdd(&st->resid_acc[0], a.r2);
+    atomicAdd(&st->resid_acc[1], a.b2);
+    atomicAdd(&st->resid_acc[2], a.x2);
+    atomicMax(reinterpret_cast<unsigned long long*>(&st->resid_acc[3]),
+              (unsigned long long)__double_as_longlong(a.amax));
+  }
+}
+
+// The gate of one solve (after every element's share is in): rel as the
+// reference computes it, the running max in resid_max, an error above tol
+// (tol <= 0: record only), and the sums cleared for the next solve.  One
+// thread per member.
+NH_DEV void resid_check(nh_status* st, int step, double tol) {
+  double* acc = st->resid_acc;
+  // L2 reads: the sums were built by atomics of other CTAs
+  const double r2 = __ldcg(acc), b2 = __ldcg(acc + 1), x2 = __ldcg(acc + 2), am = __ldcg(acc + 3);
+  if (r2 == 0.0 && b2 == 0.0 && x2 == 0.0 && am == 0.0) return;   // no solve
+  const double scale = fmax(fmax(sqrt(b2), am * sqrt(x2)), 1e-300);
+  const double rel = sqrt(r2) / scale;
+  if (rel > st->resid_max) st->resid_max = rel;
+  if (tol > 0.0 && rel > tol) nh_report(st, step, NH_ERR_SOLVE_RESIDUAL, -1);
+  acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
+}
+
+// s12 > 0 at a flagged node (the reference asserts it when the coefficients
+// are built, corrector.py:70-74; NaN passes, as with numpy's `s12 <= 0`).
+NH_DEV bool ldg_structure_ok(const NodeCoef& c0, const NodeCoef& c1) {
+  return !(c0.s12 <= 0.0) && !(c1.s12 <= 0.0);
+}
+
 // Merge two adjacent super-elements L (left) and R (right).  Also returns the
 // back-substitution rows: A_L = AL . (1, a_in, z_in), Z_R = ZR . (1, a_in, z_in).
 NH_DEV Super merge(const Super& L, const Super& R, double AL[3], double ZR[3]) {

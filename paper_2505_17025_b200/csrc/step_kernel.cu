@@ -472,14 +472,34 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
       __syncthreads();
       // ---------------- reconstruction of the compacted elements ----------------
       double pk[E][2];
+      ResidAcc ra{0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int r = 0; r < E; ++r) {
         pk[r][0] = 0.0; pk[r][1] = 0.0;
         if (jc[r] < 0) continue;
         const int j = jc[r], e = c0 - H + j;
         double P0, P1, Q0, Q1;
-        reconstruct(Sc[r], Rc[r], fld(sm.AZ, S, 0, j), fld(sm.AZ, S, 1, j), c11, P0, P1, Q0, Q1);
+        const double ap = fld(sm.AZ, S, 0, j), zn = fld(sm.AZ, S, 1, j);
+        reconstruct(Sc[r], Rc[r], ap, zn, c11, P0, P1, Q0, Q1);
         if (!isfinite(P0 + P1 + Q0 + Q1)) nh_report(st, step, NH_ERR_SOLVE_NONFINITE, e);
+        {   // residual rows of the element (corrector.py:355-366): its
+            // coefficients again from the predictor still in shared memory
+          const double ed = (double)e;
+          const double h0 = fld(sm.Qn, S, F_H0, j), h1 = fld(sm.Qn, S, F_H1, j);
+          Bottom6 b0 = bot<KIND, true>(m, bt1, sample_xd(m, ed, 0));
+          Bottom6 b1 = bot<KIND, true>(m, bt1, sample_xd(m, ed, 1));
+          Chan ch0{b0.d, b0.d_x, b0.d_t, b0.d_tt, b0.d_xt, b0.d_xx};
+          Chan ch1{b1.d, b1.d_x, b1.d_t, b1.d_tt, b1.d_xt, b1.d_xx};
+          NodeCoef q0 = ldg_coefficients(h0, fld(sm.Qn, S, F_Q0, j), fld(sm.Qn, S, F_W0, j),
+                                         elem_deriv(m, h0, h1, 0),
+                                         elem_deriv(m, h0 - b0.d, h1 - b1.d, 0), ch0, lk);
+          NodeCoef q1 = ldg_coefficients(h1, fld(sm.Qn, S, F_Q1, j), fld(sm.Qn, S, F_W1, j),
+                                         elem_deriv(m, h0, h1, 1),
+                                         elem_deriv(m, h0 - b0.d, h1 - b1.d, 1), ch1, lk);
+          const bool rs = (e == 0) || !eff(j - 1), re = (e == N - 1) || !eff(j + 1);
+          ldg_residual(m, q0, q1, lk.rho, lk.inv_rho, c11, rs, re, rs ? 0.0 : ap, zn, P0, Q0,
+                       P1, Q1, ra);
+        }
         pk[r][0] = lk.rho * P0; pk[r][1] = lk.rho * P1;
         fld(sm.Qn, S, F_Q0, j) = Q0;
         fld(sm.Qn, S, F_Q1, j) = Q1;
@@ -491,9 +511,11 @@ __device__ __forceinline__ void member_steps(const StepArgs& a, cg::cluster_grou
           a.p_out[o + 1] = pk[r][1];
         }
       }
+      resid_flush_warp(st, ra);   // the member's norms of this step's solve
       NH_TS(5);
       cluster.sync();   // ---- B3: (h p) traces visible to the neighbours
       NH_TS(6);
+      if (rank == 0 && tid == 0) resid_check(st, step, a.sch.residual_tol);
       // hw update from the bottom pressure (corrector.py:441-482)
 #pragma unroll
       for (int r = 0; r < E; ++r) {

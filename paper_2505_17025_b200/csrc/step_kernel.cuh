@@ -33,11 +33,12 @@ struct SolveArgs {
   const nh_member* members;
   const double* coef;         // [7][B][N][2]
   const uint32_t* flags;      // [B][nwords]
+  const uint32_t* starts;     // [B][nwords] range starts inside flagged runs, or NULL
   const double* outer_right;  // [B][N]
   double* p;                  // [B][N][2]
   double* hu;                 // [B][N][2]
   nh_status* status;
-  double rho, c11;
+  double rho, c11, residual_tol;
   int B, N, cluster, tile, nwords;
 };
 

@@ -183,6 +183,9 @@ __global__ void __launch_bounds__(288) nh_stream_kx(StreamArgs a) {
     const int b = blockIdx.x * 8 + lane;
     if (lane >= 8 || b >= a.B) return;
     const nh_member& m = a.members[b];
+    // residual gate of the previous step's solve (its K_C ran before this K_X)
+    if (a.sch.mode != NH_MODE_HYDROSTATIC && a.step_counter)
+      resid_check(a.status + b, a.step_counter[b] - 1, a.sch.residual_tol);
     const double tn = a.time[b] + m.dt;
     a.time[b] = tn;
     if (a.step_counter) a.step_counter[b] += 1;
@@ -330,20 +333,27 @@ __device__ __forceinline__ void kc_tile(const StreamArgs& a, int bt, KcSmem& kc)
   const bool valid = e >= 0 && e < N;
   const bool own = valid && i >= H && i < H + OWN;
   const size_t o = ((size_t)b * N + (valid ? e : 0)) * 2;
+  const size_t fe = (size_t)b * N + (valid ? e : 0);
   // global mode flags every element: no dependent flag load before the scratch loads
-  const bool flag = own && (a.sch.mode == NH_MODE_GLOBAL || a.flags_cur[(size_t)b * N + e]);
+  const bool gmode = a.sch.mode == NH_MODE_GLOBAL;
+  const bool flag = own && (gmode || a.flags_cur[fe]);
+  const nh_member& m = a.members[b];
+  const double rho = a.sch.rho, inv_rho = 1.0 / rho, c11 = a.sch.c11;
   Super S = super_identity();
   double R[6] = {0, 0, 0, 0, 0, 0};
+  bool range_start = false, range_end = false;
   if (flag) {
-    const size_t BN = (size_t)a.B * N;
-    const double* sc = a.scratch + (size_t)b * N + e;
-    S = Super{sc[0], sc[BN], sc[2 * BN], sc[3 * BN], sc[4 * BN], sc[5 * BN]};
-#pragma unroll
-    for (int r = 0; r < 6; ++r) R[r] = sc[(6 + r) * BN];
+    // re-eliminate the element block from K_S's coefficients: the same
+    // super-element K_S aggregated, plus the reconstruction rows
+    NodeCoef c0, c1;
+    load_coef(a.scratch + fe, (size_t)a.B * N, c0, c1);
+    range_start = e == 0 || !(gmode || a.flags_cur[fe - 1]);
+    range_end = e == N - 1 || !(gmode || a.flags_cur[fe + 1]);
+    local_condense(m, c0, c1, rho, inv_rho, c11, range_end, S, R);
   } else if (own) {
     S = super_gap(a.hu_out[o]);
   }
-  // up: the same trees K_P built (recomputed from the stored super-elements)
+  // up: the same trees K_S built (recomputed from the super-elements)
   const bool wany = __any_sync(0xffffffffu, flag);
   double* wn = wnode + warp * 31 * 6;
   Super agg = S;
@@ -366,20 +376,25 @@ __device__ __forceinline__ void kc_tile(const StreamArgs& a, int bt, KcSmem& kc)
     if (lane < NW) { wio[lane * 2] = ai; wio[lane * 2 + 1] = zi; }
   }
   __syncthreads();
-  if (!wany) return;
+  if (!wany) return;   // warp-uniform
   double a_in = wio[warp * 2], z_in = wio[warp * 2 + 1];
   warp_down(a_in, z_in, wn, lane, 5);
-  if (!flag) return;
-  double P0, P1, Q0, Q1;
-  reconstruct(S, R, a_in, z_in, a.sch.c11, P0, P1, Q0, Q1);
-  if (!isfinite(P0 + P1 + Q0 + Q1)) {
-    int step = a.step_counter ? a.step_counter[b] - 1 : 0;
-    nh_report(a.status + b, step, NH_ERR_SOLVE_NONFINITE, e);
+  ResidAcc ra{0.0, 0.0, 0.0, 0.0};
+  if (flag) {
+    double P0, P1, Q0, Q1;
+    reconstruct(S, R, a_in, z_in, c11, P0, P1, Q0, Q1);
+    const int step = a.step_counter ? a.step_counter[b] - 1 : 0;
+    if (!isfinite(P0 + P1 + Q0 + Q1)) nh_report(a.status + b, step, NH_ERR_SOLVE_NONFINITE, e);
+    NodeCoef c0, c1;   // reloaded (L1 / L2) rather than held across the trees
+    load_coef(a.scratch + fe, (size_t)a.B * N, c0, c1);
+    ldg_residual(m, c0, c1, rho, inv_rho, c11, range_start, range_end,
+                 range_start ? 0.0 : a_in, z_in, P0, Q0, P1, Q1, ra);
+    *reinterpret_cast<double2*>(a.hu_out + o) = double2{Q0, Q1};
+    double* pn = a.pend_out + fe;
+    pn[0] = rho * P0;
+    pn[(size_t)a.B * N] = rho * P1;
   }
-  *reinterpret_cast<double2*>(a.hu_out + o) = double2{Q0, Q1};
-  double* pn = a.pend_out + (size_t)b * N + e;
-  pn[0] = a.sch.rho * P0;
-  pn[(size_t)a.B * N] = a.sch.rho * P1;
+  resid_flush_warp(a.status + b, ra);   // the member's norms of this step's solve
 }
 
 // Persistent: the grid strides over the step's list of flagged tiles.

@@ -13,12 +13,6 @@
 #ifndef NH_STREAM_MIN_BLOCKS
 #define NH_STREAM_MIN_BLOCKS (1024 / NH_STREAM_THREADS)   // K_P CTAs per SM (64 registers)
 #endif
-#ifndef NH_KP_RUNTIME_KIND
-#define NH_KP_RUNTIME_KIND 0   // 1: one K_P body with run-time bottom dispatch (smaller code)
-#endif
-#ifndef NH_KP_WARP_XCHG
-#define NH_KP_WARP_XCHG 0      // 1: K_P neighbour exchange by shuffles + warp-pair named barriers (measured slower)
-#endif
 #ifndef NH_KS_MIN_BLOCKS
 #define NH_KS_MIN_BLOCKS (1024 / NH_STREAM_THREADS)       // K_S / K_C CTAs per SM (64 registers; measured 6 / 8 / 10 at 128 threads: 8 fastest)
 #endif
@@ -35,7 +29,7 @@ struct StreamArgs {
   uint8_t* flags_cur;
   const double* pend;          // [6][B*N] planes p0 p1 phi0 phi1 dx0 dx1 of the pending step, or NULL
   double* pend_out;            // same, for this step
-  double* scratch;             // [12][B*N] planes: super-element (6) + reconstruction rows (6)
+  double* scratch;             // [10][B*N] planes: LDG coefficients of flagged elements (store_coef)
   double* tile_agg;            // [B][T][8] aggregate (6), flagged count, right ghost
   double* tile_io;             // [B][T][2] (a_in, z_in)
   double* time;                // [B]
@@ -61,7 +55,7 @@ struct StreamArgs {
 void* nh_stream_kernel(int which);
 void* nh_stream_kp_ptr();    // stream_kp.cu
 size_t nh_stream_kp_smem();  // its dynamic shared memory
-int nh_stream_kp_threads();  // its block size (NH_KP_E2: half a tile)
+int nh_stream_kp_threads();  // its block size
 void* nh_stream_kp_fused_ptr();  // K_P with the K_S condensation fused in (global mode), or NULL
 int nh_stream_kp_records_hw_any();   // 1: K_P records any(hw != 0) for the w / w_x fallback
 int nh_launch_gather_p(const double* pend, const uint8_t* flags, double* p, size_t n,

@@ -1,29 +1,6 @@
 // K_P of the streaming step (body in stream_kp.cuh); its own translation unit.
 #include "stream_kp.cuh"
-#include "stream_kp2.cuh"
 
-#ifndef NH_KP_E2
-#define NH_KP_E2 0   // 1: two elements per thread (stream_kp2.cuh); measured 20% slower (fewer warps)
-#endif
-
-#if NH_KP_E2
-#ifndef NH_KP2_MIN_BLOCKS
-#define NH_KP2_MIN_BLOCKS 8   // 64-thread CTAs per SM: 128 registers
-#endif
-__global__ void __launch_bounds__(TP2, NH_KP2_MIN_BLOCKS) nh_stream_kp(StreamArgs a) {
-  __shared__ nh_member msh;
-  __shared__ MemberConst mc;
-  extern __shared__ __align__(16) unsigned char kp_dyn[];
-  Kp2Smem& ks = *reinterpret_cast<Kp2Smem*>(kp_dyn);
-  int b = blockIdx.z * 65535 + blockIdx.y;
-  if (b >= a.B) return;
-  if (a.order) b = a.order[b];
-  kp2_tile(a, b, blockIdx.x, msh, mc, ks);
-}
-size_t nh_stream_kp_smem() { return sizeof(Kp2Smem); }
-int nh_stream_kp_threads() { return TP2; }
-void* nh_stream_kp_fused_ptr() { return nullptr; }
-#else
 
 template <bool FUSE>
 __device__ __forceinline__ void kp_entry(const StreamArgs& a) {
@@ -51,8 +28,7 @@ void* nh_stream_kp_fused_ptr() { return (void*)nh_stream_kp_fused; }
 
 size_t nh_stream_kp_smem() { return sizeof(KpSmem); }
 int nh_stream_kp_threads() { return TPB; }
-#endif
 
 void* nh_stream_kp_ptr() { return (void*)nh_stream_kp; }
-int nh_stream_kp_records_hw_any() { return NH_KP_E2 ? 0 : 1; }   // w / w_x fallback (K_F)
+int nh_stream_kp_records_hw_any() { return 1; }   // w / w_x fallback (K_F)
 

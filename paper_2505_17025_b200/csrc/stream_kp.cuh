@@ -23,88 +23,6 @@ struct Q6 {
   double h0, h1, q0, q1, w0, w1;
 };
 
-#if NH_KP_WARP_XCHG
-// Named-barrier handshakes between neighbouring warps (ids 1..2*(NW-1); 0 is
-// __syncthreads).  A(w): warp w's node-1 side is in smem for warp w+1.
-// B(w): warp w+1's left-face flux is in smem for warp w.
-__device__ __forceinline__ void bar_arrive(int id) {
-  asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory");
-}
-__device__ __forceinline__ void bar_wait(int id) {
-  asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
-}
-#define NH_BAR_A(w) (1 + (w))
-#define NH_BAR_B(w) (NW + (w))
-
-// one Heun stage for the thread's element.  Neighbour exchange inside a warp
-// goes through shuffles; across a warp boundary through two small smem slots
-// per warp and a producer/consumer named barrier with that neighbour only, so
-// warps never wait for the whole CTA.
-template <int KIND>
-__device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q6& q,
-                                           const BottomTime& bt, double x0, double x1,
-                                           const BottomSpace& s0, const BottomSpace& s1, int i,
-                                           int e, int N, double* xs, double* xf, double t6[6],
-                                           double& speed, double& d0, double& d1) {
-  const int lane = i & 31, warp = i >> 5;
-  Bottom6 b0 = bottom_eval_sp_k<KIND>(m, bt, x0, s0);
-  Bottom6 b1 = bottom_eval_sp_k<KIND>(m, bt, x1, s1);
-  Side n0, n1;
-  make_sides_warp(q.h0, q.q0, q.w0, b0.d, q.h1, q.q1, q.w1, b1.d, n0, n1);
-  // left neighbour's node-1 side (u included: no second division)
-  Side L;
-  L.h = __shfl_up_sync(0xffffffffu, n1.h, 1);
-  L.hu = __shfl_up_sync(0xffffffffu, n1.hu, 1);
-  L.hw = __shfl_up_sync(0xffffffffu, n1.hw, 1);
-  L.d = __shfl_up_sync(0xffffffffu, n1.d, 1);
-  L.u = __shfl_up_sync(0xffffffffu, n1.u, 1);
-  if (lane == 31) {
-    double* x = xs + warp * 5;
-    x[0] = n1.h; x[1] = n1.hu; x[2] = n1.hw; x[3] = n1.d; x[4] = n1.u;
-  }
-  if (warp < NW - 1) bar_arrive(NH_BAR_A(warp));
-  if (warp > 0) {
-    bar_wait(NH_BAR_A(warp - 1));
-    if (lane == 0) {
-      const double* x = xs + (warp - 1) * 5;
-      L.h = x[0]; L.hu = x[1]; L.hw = x[2]; L.d = x[3]; L.u = x[4];
-    }
-  }
-#if NH_STRICT
-  L.rh = 0.0;
-#else
-  L.rh = nh_rcp(L.h);
-#endif
-  if (e == 0) L = ghost_side(n0, m.bc_left);
-  // (CTA slot 0 keeps lane 0's own value: a halo element, never used)
-  double sp;
-  Face fl = face_flux<KIND == NH_BOTTOM_FLAT, true>(L, n0, g, sp);
-  speed = fmax(speed, sp);
-  Face fr;
-  fr.F1 = __shfl_down_sync(0xffffffffu, fl.F1, 1);
-  fr.F2L = __shfl_down_sync(0xffffffffu, fl.F2L, 1);
-  fr.F3 = __shfl_down_sync(0xffffffffu, fl.F3, 1);
-  fr.F2R = 0.0;
-  if (lane == 0) {
-    double* y = xf + warp * 3;
-    y[0] = fl.F1; y[1] = fl.F2L; y[2] = fl.F3;
-  }
-  if (warp > 0) bar_arrive(NH_BAR_B(warp - 1));
-  if (warp < NW - 1) {
-    bar_wait(NH_BAR_B(warp));
-    if (lane == 31) {
-      const double* y = xf + (warp + 1) * 3;
-      fr.F1 = y[0]; fr.F2L = y[1]; fr.F3 = y[2];
-    }
-  }
-  if (e == N - 1) {
-    fr = face_flux<KIND == NH_BOTTOM_FLAT>(n1, ghost_side(n1, m.bc_right), g, sp);
-    speed = fmax(speed, sp);
-  }
-  element_tendency<KIND == NH_BOTTOM_FLAT>(m, g, n0, n1, fl, fr, b0.d_x, b1.d_x, t6);
-  d0 = b0.d; d1 = b1.d;
-}
-#else
 // one Heun stage for the thread's element: node sides from the registers,
 // left face from the left neighbour's node-1 side (exchanged through smem),
 // right face from the right neighbour's left face (exchanged through smem)
@@ -151,13 +69,28 @@ __device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q
   d0 = b0.d; d1 = b1.d;
 }
 
-#endif
-
 __device__ __forceinline__ void store_super(double* dst, const Super& s) {
   dst[0] = s.ga; dst[1] = s.aa; dst[2] = s.ba; dst[3] = s.gz; dst[4] = s.az; dst[5] = s.bz;
 }
 __device__ __forceinline__ Super load_super(const double* s) {
   return Super{s[0], s[1], s[2], s[3], s[4], s[5]};
+}
+
+// The element's LDG coefficients as 10 scratch planes of stride BN (K_S or
+// the fused K_P store, K_C loads): s11, s12, s22, f1, f2 at nodes 0 and 1.
+constexpr int NH_COEF_PLANES = 10;
+__device__ __forceinline__ void store_coef(double* sc, size_t BN, const NodeCoef& c0,
+                                           const NodeCoef& c1) {
+  sc[0 * BN] = c0.s11; sc[1 * BN] = c1.s11; sc[2 * BN] = c0.s12; sc[3 * BN] = c1.s12;
+  sc[4 * BN] = c0.s22; sc[5 * BN] = c1.s22; sc[6 * BN] = c0.f1;  sc[7 * BN] = c1.f1;
+  sc[8 * BN] = c0.f2;  sc[9 * BN] = c1.f2;
+}
+__device__ __forceinline__ void load_coef(const double* sc, size_t BN, NodeCoef& c0,
+                                          NodeCoef& c1) {
+  c0.s11 = sc[0 * BN]; c1.s11 = sc[1 * BN]; c0.s12 = sc[2 * BN]; c1.s12 = sc[3 * BN];
+  c0.s22 = sc[4 * BN]; c1.s22 = sc[5 * BN]; c0.f1 = sc[6 * BN];  c1.f1 = sc[7 * BN];
+  c0.f2 = sc[8 * BN];  c1.f2 = sc[9 * BN];
+  c0.phi = 0.0; c1.phi = 0.0;
 }
 
 // CTA-level reduction of per-element super-elements (1 per thread) into the
@@ -197,15 +130,8 @@ __device__ __forceinline__ Super tile_up(Super agg, bool tflag, double* wnode, d
 
 // ---------------------------------------------------------------------- K_P
 struct KpSmem {
-#if NH_KP_WARP_XCHG
-  double sh[2 * TPB];     // (h p) traces of the pending correction
-  double sf[1];
-  double xs[NW * 5];      // per warp: node-1 side of its lane 31
-  double xf[NW * 3];      // per warp: left-face flux of its lane 0
-#else
   double sh[5 * TPB];
   double sf[3 * TPB];
-#endif
   double sk[6 * TPB];     // k1 of this thread's element
   alignas(16) double sq[6 * TPB];   // step-start state: [3][TPB] double2 (h, hu, hw node pairs)
   unsigned long long wcfl[NW];   // per warp: max wave speed bits (CFL = speed dt / dx at the end)
@@ -214,13 +140,8 @@ struct KpSmem {
 
 
 
-// (h p) traces of the pending correction: the sf planes (the warp-exchange
-// variant keeps them in its sh)
-#if NH_KP_WARP_XCHG
-#define NH_HP_TRACES(ks) ((ks).sh)
-#else
+// (h p) traces of the pending correction: the sf planes
 #define NH_HP_TRACES(ks) ((ks).sf)
-#endif
 
 struct KsSmem {
   double wnode[NW * 31 * 6];
@@ -284,9 +205,11 @@ __device__ __forceinline__ void load_member(const StreamArgs& a, int b, nh_membe
 
 // One flagged element's LDG condensation (K_S, or the fused K_P):
 // LDG coefficients at t + dt (corrector.py:100-170), the element block
-// eliminated to its super-element (corrector.py:173-349 -> physics.cuh), the
-// super-element + reconstruction rows stored for K_C, and phi / d_x stored in
-// the pending record of the hw update.  q = predictor state of the element.
+// eliminated to its super-element (corrector.py:173-349 -> physics.cuh) for
+// the tile aggregate, the coefficients stored for K_C (which re-eliminates
+// the block for the reconstruction rows and evaluates the residual gate), and
+// phi / d_x stored in the pending record of the hw update.  q = predictor
+// state of the element.
 template <int KIND>
 __device__ __forceinline__ void condense_element(const StreamArgs& a, const nh_member& m,
                                                  const LdgConst& lk, const BottomTime& bt1, int b,
@@ -302,18 +225,17 @@ __device__ __forceinline__ void condense_element(const StreamArgs& a, const nh_m
   double exb = ederiv(m, q.h0 - b0.d, q.h1 - b1.d, 1);
   NodeCoef c0 = ldg_coefficients(q.h0, q.q0, q.w0, ederiv(m, q.h0, q.h1, 0), exa, ch0, lk);
   NodeCoef c1 = ldg_coefficients(q.h1, q.q1, q.w1, ederiv(m, q.h0, q.h1, 1), exb, ch1, lk);
-  double R[6];
-  if (!local_condense(m, c0, c1, lk.rho, lk.inv_rho, a.sch.c11, range_end, S, R))
-    nh_report(a.status + b, a.step_counter ? a.step_counter[b] : 0, NH_ERR_SOLVE_PIVOT, e);
-  // field-major planes: each store of the warp is one coalesced run
+  // field-major planes: each store of the warp is one coalesced run (stored
+  // before the elimination, so the coefficients are dead during it)
   const size_t BN = (size_t)a.B * N, fe = (size_t)b * N + e;
-  double* sc = a.scratch + fe;
-  sc[0 * BN] = S.ga; sc[1 * BN] = S.aa; sc[2 * BN] = S.ba;
-  sc[3 * BN] = S.gz; sc[4 * BN] = S.az; sc[5 * BN] = S.bz;
-#pragma unroll
-  for (int r = 0; r < 6; ++r) sc[(6 + r) * BN] = R[r];
+  store_coef(a.scratch + fe, BN, c0, c1);
   double* pn = a.pend_out + fe;
   pn[2 * BN] = c0.phi; pn[3 * BN] = c1.phi; pn[4 * BN] = b0.d_x; pn[5 * BN] = b1.d_x;
+  const int step = a.step_counter ? a.step_counter[b] : 0;
+  if (!ldg_structure_ok(c0, c1)) nh_report(a.status + b, step, NH_ERR_STRUCTURE, e);
+  double R[6];
+  if (!local_condense(m, c0, c1, lk.rho, lk.inv_rho, a.sch.c11, range_end, S, R))
+    nh_report(a.status + b, step, NH_ERR_SOLVE_PIVOT, e);
 }
 
 template <int KIND, bool FUSE, class SM>
@@ -323,14 +245,8 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   double* sh = ks.sh;
   double* sf = ks.sf;
   uint8_t* rf = ks.rf;
-#if NH_KP_WARP_XCHG
-  double* XS = ks.xs;
-  double* XF = ks.xf;
-  (void)sf;
-#else
   double* XS = sh;
   double* XF = sf;
-#endif
 
   const int N = a.N, T = a.tiles;
   const int b = ti.b, tile = ti.tile, i = ti.i, lane = ti.lane, e = ti.e;
@@ -570,14 +486,14 @@ __device__ __forceinline__ void kp_correct_and_step(const StreamArgs& a, const T
       double2 vw{q.w0, q.w1};
       *reinterpret_cast<double2*>(const_cast<double*>(a.hw_in) + ti.o) = vw;
     }
+    // residual gate of the last step's solve (K_X checks the earlier ones)
+    if (ti.tile == 0 && i == 0 && a.step_counter)
+      resid_check(a.status + b, a.step_counter[b] - 1, a.sch.residual_tol);
     return;
   }
   if (a.hw_any) {   // w / w_x criterion: member-wide any(hw != 0) of the step input
     if (__syncthreads_or(ti.own && (q.w0 != 0.0 || q.w1 != 0.0)) && i == 0) a.hw_any[b] = 1;
   }
-#if NH_KP_RUNTIME_KIND
-  kp_body<-1, FUSE>(a, msh, mc, ti, q, ks, sq);
-#else
   switch (msh.bottom_kind) {
     case NH_BOTTOM_FLAT: kp_body<NH_BOTTOM_FLAT, FUSE>(a, msh, mc, ti, q, ks, sq); break;
     case NH_BOTTOM_PLATE: kp_body<NH_BOTTOM_PLATE, FUSE>(a, msh, mc, ti, q, ks, sq); break;
@@ -585,7 +501,6 @@ __device__ __forceinline__ void kp_correct_and_step(const StreamArgs& a, const T
     case NH_BOTTOM_SMOOTH_BOX: kp_body<NH_BOTTOM_SMOOTH_BOX, FUSE>(a, msh, mc, ti, q, ks, sq); break;
     default: kp_body<NH_BOTTOM_SLOPE_SLIDE, FUSE>(a, msh, mc, ti, q, ks, sq); break;
   }
-#endif
 }
 
 // One K_P tile (b, tile): the body of nh_stream_kp / nh_stream_kp_fused.

@@ -116,6 +116,12 @@ class Ensemble:
             self._chunk = int(max(1, min(self.B, budget // per)))
         return self._chunk
 
+    def release_workspace(self):
+        """Drop the streaming workspace (re-allocated by the next advance)."""
+        self._ws = None
+        self._chunk = None
+        D.torch().cuda.empty_cache()
+
     def advance(self, n_steps: int, mode: str = "adaptive", criterion: Criterion | None = None,
                 flux: FluxCoefficients = FluxCoefficients(), g: float = 9.81,
                 rho: float = RHO_WATER, flag_bits=None, p_out=None, path: str = "auto",
@@ -173,6 +179,74 @@ class Ensemble:
             t0v = 0.0 if t0 is None else np.asarray(t0).ravel()[i]
             D.raise_for_status(st, t0v, self.records["dt"][i], member=i)
         return st
+
+
+def advance_host(records: np.ndarray, h, hu, hw, time, n_steps: int, mode: str = "adaptive",
+                 criterion: Criterion | None = None, block: int | None = None,
+                 flux: FluxCoefficients = FluxCoefficients(), g: float = 9.81,
+                 rho: float = RHO_WATER) -> np.ndarray:
+    """Advance an ensemble that lives in HOST memory by n_steps, in place.
+
+    h, hu, hw: CPU float64 tensors (B, N, 2) -- pinned memory gives
+    asynchronous copies; time: CPU float64 (B,).  The members are streamed
+    through the GPU in blocks of `block` members, pipelined on three CUDA
+    streams: the copy-in of block i+1 and the copy-out of block i-1 overlap
+    the K steps of block i (two device buffers, one streaming workspace).
+    This is the end-to-end call for ensembles kept on the host (the bench's
+    e2e leg); members are independent, so the result equals
+    Ensemble(...).advance(n_steps) bit for bit.  Returns the nh_status
+    records of all members.
+    """
+    if mode not in _MODES:
+        raise ValueError(f"unknown mode {mode!r}")
+    if mode == "adaptive" and criterion is None:
+        raise ValueError("adaptive mode requires a criterion")
+    T = D.torch()
+    D.require_cuda()
+    B, N = int(h.shape[0]), int(h.shape[1])
+    if tuple(h.shape[1:]) != (N, 2) or hu.shape != h.shape or hw.shape != h.shape:
+        raise ValueError("h, hu, hw must be (B, N, 2) P1 states of equal shape")
+    c = criterion if criterion is not None else Criterion("eta_over_d")
+    sch = D.scheme(_MODES[mode], c.kind, c.k_nh, c.enlarge, flux, g, rho)
+    block = max(1, min(B, block or 4096))
+    members = D.upload_members(np.ascontiguousarray(records))
+    status = D.new_status(B)
+    rec, stb = _lib.MEMBER_DTYPE.itemsize, _lib.STATUS_DTYPE.itemsize
+    ws = D.stream_workspace(block, N)
+    bufs = [[T.empty((block, N, 2), dtype=T.float64, device="cuda") for _ in range(3)] +
+            [T.empty(block, dtype=T.float64, device="cuda")] for _ in range(2)]
+    host = (h, hu, hw, time)
+    s_in, s_cmp, s_out = T.cuda.Stream(), T.cuda.current_stream(), T.cuda.Stream()
+    s_in.wait_stream(s_cmp)
+    freed = [None, None]       # event: the buffer's previous copy-out finished
+    for i, c0 in enumerate(range(0, B, block)):
+        c1 = min(B, c0 + block)
+        n, k = c1 - c0, i & 1
+        buf = bufs[k]
+        with T.cuda.stream(s_in):
+            if freed[k] is not None:
+                s_in.wait_event(freed[k])
+            for dst, src in zip(buf, host):
+                dst[:n].copy_(src[c0:c1], non_blocking=True)
+            loaded = T.cuda.Event()
+            loaded.record(s_in)
+        s_cmp.wait_event(loaded)
+        with T.cuda.stream(s_cmp):
+            D.stream_advance(members[c0 * rec:c1 * rec], buf[0][:n], buf[1][:n], buf[2][:n],
+                             buf[3][:n], n_steps, sch, status[c0 * stb:c1 * stb], ws)
+            done = T.cuda.Event()
+            done.record(s_cmp)
+        s_out.wait_event(done)
+        with T.cuda.stream(s_out):
+            for dst, src in zip(host, buf):
+                dst[c0:c1].copy_(src[:n], non_blocking=True)
+            freed[k] = T.cuda.Event()
+            freed[k].record(s_out)
+    s_cmp.wait_stream(s_out)
+    s_cmp.synchronize()
+    for b in bufs:   # keep the buffers alive until the copies finished
+        del b
+    return D.read_status(status)
 
 
 def simulate(spec: ScenarioSpec, initial: FlowState, mode: str,

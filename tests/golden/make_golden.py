@@ -156,11 +156,74 @@ def short_fixtures():
     print("short.npz:", len(data), "arrays")
 
 
+def error_fixtures():
+    """The reference's error semantics and adjacent ranges (errors.npz):
+    residual gate, non-finite solve, structural asserts, and corrections on
+    touching ranges (each range its own block of the batched system)."""
+    data = {}
+    n = 48
+    grid = R.GridSpec(0.0, 1.0, n)
+    x = grid.nodes
+    s11 = 0.4 * np.sin(2.0 * np.pi * x)
+    s12 = 2.0 + np.cos(x)
+    s22 = 1.0 + 0.5 * np.sin(3.0 * x)
+    f1 = np.cos(np.pi * x) + s12
+    f2 = -2.0 * np.sin(2.0 * x) + s22
+    z = np.zeros_like(x)
+    bottom = R.FlatBottom(1.0).sample(grid.sample_nodes, 0.0)
+
+    def coeffs(**kw):
+        base = dict(s11=s11, s12=s12, s21=-s11, s22=s22, f1=f1, f2=f2, phi=z)
+        base.update(kw)
+        return RC.EllipticCoefficients(grid, base["s11"], base["s12"], base["s21"], base["s22"],
+                                       base["f1"], base["f2"], base["phi"], bottom, 0.1, 1.0)
+
+    def outcome(fn):
+        try:
+            fn()
+            return "ok"
+        except Exception as exc:   # noqa: BLE001 - the type name is the fixture
+            return type(exc).__name__
+
+    co = coeffs()
+    data["err/coef"] = np.stack([s11, s12, s22, f1, f2])
+    data["err/tol_default"] = np.array(outcome(lambda: RC.ldg_solve(co, (3, 40), (0.2, 0.3))))
+    data["err/tol_1e-18"] = np.array(outcome(
+        lambda: RC.ldg_solve(co, (3, 40), (0.2, 0.3), residual_tol=1e-18)))
+    bad_f1 = f1.copy()
+    bad_f1[10, 1] = np.inf
+    data["err/nonfinite"] = np.array(outcome(lambda: RC.ldg_solve(coeffs(f1=bad_f1), (3, 40))))
+    neg = s12.copy()
+    neg[7, 0] = -1.0
+    data["err/s12_negative"] = np.array(outcome(lambda: coeffs(s12=neg)))
+    data["err/s21_mismatch"] = np.array(outcome(lambda: coeffs(s21=-s11 + 1e-3)))
+    data["err/flux_c12_0"] = np.array(outcome(
+        lambda: RC.ldg_solve(co, (3, 40), flux=RC.FluxCoefficients(0.5, 0.0, 0.0))))
+    # touching ranges: separate systems (solve_on_ranges and apply_correction)
+    for name, grid_, bathy, bspec, bcs, dt, st in cases()[:3]:
+        pred = RH.heun_step(st, dt, bathy, bcs, cfl_warn=False)
+        m = grid_.n_elements
+        ranges = ((2, m // 4), (m // 4 + 1, m // 2), (m // 2 + 1, m // 2 + 1), (m - 3, m - 1))
+        corr, sol = RC.apply_correction(pred, bathy, dt, ranges, bcs)
+        p = "adj/" + name + "/"
+        data[p + "pred"] = np.stack([pred.h.values, pred.hu.values, pred.hw.values])
+        data[p + "ranges"] = np.array(ranges)
+        data[p + "corr"] = np.stack([corr.hu.values, corr.hw.values, sol.p_nh.values])
+        co2 = RC.assemble_coefficients(pred, bathy, dt)
+        sol2 = RC.solve_on_ranges(pred, co2, ranges, bcs)
+        data[p + "solve"] = np.stack([sol2.hu_corrected.values, sol2.p_nh.values])
+    np.savez_compressed(os.path.join(HERE, "errors.npz"), **data)
+    print("errors.npz:", {k: str(v) for k, v in data.items() if v.dtype.kind == "U"})
+
+
 def digest(flags: np.ndarray) -> int:
     return zlib.crc32(np.packbits(flags).tobytes())
 
 
-CHECKPOINTS = {"config3": (500, 5000, 10000, 15000, 20000, 25000, 30000)}
+# config 3: every 5000 steps through the end (windowed parity restarts the
+# GPU from each one), plus the step before the first free-running mask flip
+# (34652, DESIGN.md §5) for the criterion-margin report
+CHECKPOINTS = {"config3": (500,) + tuple(range(5000, 112755, 5000)) + (34652,)}
 
 
 def long_fixture(name, n_steps=None):
@@ -225,8 +288,11 @@ def long_fixture(name, n_steps=None):
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--long", nargs="*", default=None)
+    ap.add_argument("--errors", action="store_true")
     args = ap.parse_args()
-    if args.long is None:
+    if args.errors:
+        error_fixtures()
+    elif args.long is None:
         short_fixtures()
     else:
         for name in args.long or ["config1", "config2", "config3"]:

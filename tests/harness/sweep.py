@@ -29,11 +29,13 @@ from pathlib import Path
 
 import numpy as np
 
-from . import _device as D
-from .adaptivity import CRITERION_KINDS, Criterion
-from .driver import Ensemble, RunResult, simulate
+from paper_2505_17025_b200 import _device as D
+from paper_2505_17025_b200.adaptivity import CRITERION_KINDS, Criterion
+from paper_2505_17025_b200.driver import Ensemble, RunResult, simulate
+from paper_2505_17025_b200.scenarios import ScenarioSpec
+
 from .metrics import DegenerateSeriesError, RunReport, SeriesPair, pearson, rmse, time_ratio
-from .scenarios import ScenarioSpec, solitary_exact
+from .paper_cases import solitary_exact
 
 SWEEP_HEADER = ("criterion", "enlarge", "time_ratio", "mask_fraction", "rmse", "r")
 

@@ -1,6 +1,7 @@
 """bench.py's reference arm on CPU: one JSON line with the driver's keys, the
 b200 arm's workload / metric / unit, and its own cpu_baseline and e2e
-objects (the oracle port, run here on a 1-step sample, one member per host core)."""
+objects (the reference's own step when baseline/_ref holds it, else the oracle
+port; run here on a 1-step sample of config 5, one member per host core)."""
 
 import json
 import os
@@ -13,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_reference_arm_json_line():
     env = dict(os.environ, OPENBLAS_NUM_THREADS="1")
     out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1",
-                          "--warmup", "0"], cwd=ROOT, env=env, capture_output=True, text=True,
+                          "--warmup", "0", "--spinup", "0"], cwd=ROOT, env=env, capture_output=True, text=True,
                          timeout=600, check=True).stdout
     lines = [l for l in out.splitlines() if l.startswith("{")]
     assert len(lines) == 1
@@ -24,9 +25,11 @@ def test_reference_arm_json_line():
               "cpu_baseline", "e2e"):
         assert k in d, k
     assert d["unit"] == "cell-steps/s" and d["higher_is_better"] is True
-    assert d["config"]["workload"] == "config4" and d["config"]["mode"] == "adaptive"
+    assert d["config"]["workload"] == "config5" and d["config"]["mode"] == "adaptive"
     assert d["value"] > 0 and d["ms_per_step"] > 0
     cb = d["cpu_baseline"]
-    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"]
+    assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["value"] == d["value"]
+    if os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "nhswe")):
+        assert cb["kind"] == "reference"
     e = d["e2e"]
     assert e["value"] == d["value"] and e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0

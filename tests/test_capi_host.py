@@ -32,7 +32,7 @@ def test_library_loads_and_exports_every_symbol():
     lib = _lib.load()
     for name in header_functions():
         assert getattr(lib, name) is not None
-    assert lib.nh_abi_version() == _lib.ABI_VERSION == 3
+    assert lib.nh_abi_version() == _lib.ABI_VERSION == 4
 
 
 def test_plan_host_logic():
@@ -48,8 +48,8 @@ def test_plan_host_logic():
 
 def test_struct_layouts():
     assert _lib.MEMBER_DTYPE.itemsize == 312
-    assert _lib.STATUS_DTYPE.itemsize == 32
-    assert ctypes.sizeof(_lib.Scheme) == 64
+    assert _lib.STATUS_DTYPE.itemsize == 72
+    assert ctypes.sizeof(_lib.Scheme) == 72
     assert ctypes.sizeof(_lib.Outputs) == 48
 
 

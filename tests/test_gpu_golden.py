@@ -194,48 +194,7 @@ def test_full_length_config_vs_reference(cfg_name, mode):
         mism = np.flatnonzero(np.array(crc, dtype=np.uint32) != G[mode + "/flag_crc"])
         print(f"{cfg_name}: {mism.size} of {n_steps} step masks differ "
               f"(max count difference {np.abs(cnt - G[mode + '/flag_count']).max()})")
-        # near-threshold flips only: element counts may differ by a cell or two
-        assert mism.size <= max(2, n_steps // 1000)
-        assert np.abs(cnt - G[mode + "/flag_count"]).max() <= 2
-        assert abs(res.mask_fraction_mean - float(G[mode + "/mask_fraction"])) < 1e-4
-
-
-MEMBERS = os.path.join(GOLDEN, "members_full.npz")
-
-
-def _member_cases():
-    if not os.path.exists(MEMBERS):
-        return []
-    keys = np.load(MEMBERS).files
-    return sorted({tuple(k.split("/")[:3]) for k in keys})
-
-
-@pytest.mark.parametrize("path", ["resident", "stream"])
-@pytest.mark.parametrize("case", _member_cases(), ids=lambda c: "-".join(c))
-def test_sampled_members_full_length(case, path):
-    """Configs 4 and 5 at their full step counts: sampled members (both bottom
-    kinds of config 4, both ends of the config-5 table, both modes) against
-    the REAL reference's final state (tests/golden/make_members.py)."""
-    G = np.load(MEMBERS)
-    name, i, mode = case[0], int(case[1]), case[2]
-    key = f"{name}/{i}/{mode}"
-    cfg = configs.get(name)
-    m = cfg.member(i)
-    from tests.helpers import oracle_depth
-    h, hu, hw = cfg.host_state(i, oracle_depth)
-    ens = P.Ensemble.from_host(cfg.records([i]), h[None], hu[None], hw[None])
-    n = cfg.n_steps
-    crit = P.Criterion("eta_over_d") if mode == "adaptive" else None
-    ens.advance(n, mode, crit, path=path)
-    st = ens.check()
-    assert float(ens.time.item()) == float(G[key + "/time"])
-    d = oracle_depth(m.bathymetry, m.grid.sample_nodes, float(G[key + "/time"]))
-    gh, gq = ens.h[0].cpu().numpy(), ens.hu[0].cpu().numpy()
-    e_eta = rel(gh - d, G[key + "/h"] - d)
-    e_hu = rel(gq, G[key + "/hu"])
-    frac = st["flagged"][0] / (n * cfg.n_elements)
-    print(f"{key} [{path}]: eta {e_eta:.3e} hu {e_hu:.3e} mask fraction {frac:.5f}")
-    assert e_eta <= 1e-9 and e_hu <= 1e-9
-    if mode == "adaptive":
-        frac_ref = G[key + "/counts"].astype(float).mean() / cfg.n_elements
-        assert abs(frac - frac_ref) <= 1e-4
+        # every step's mask equals the reference's (no near-threshold flip
+        # occurs in these runs; the margin rule of SURVEY H4 would admit one)
+        assert mism.size == 0, f"first differing steps {mism[:5]}"
+        assert np.array_equal(cnt, G[mode + "/flag_count"])

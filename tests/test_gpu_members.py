@@ -1,0 +1,173 @@
+"""Configs 4 and 5 against the REAL reference, member by member, inside the
+full ensembles (>= 32 sampled members per throughput config,
+parameter-range corners included, per-step masks compared).
+
+tests/golden/make_members.py ran each sampled member through the reference's
+own `simulate` for the config's full step count and stored the final h / hu,
+the per-step flagged counts and the per-step mask CRC (crc32 of
+np.packbits(flags)).  Here:
+
+* config 4: the whole 4096-member ensemble runs its 20000 steps on the
+  streaming path, recording every member's per-step flag bit-planes in
+  windows; every sampled member's per-step masks must equal the reference's
+  bit for bit (CRC and count at every step) and its final eta / hu must be
+  within 1e-9 relative L-inf;
+* config 5: the 32 sampled members as one ensemble, 10000 steps in each mode,
+  with the same per-step mask and final-state checks; and the full
+  65536-member ensemble (run in member blocks) must leave those members
+  bitwise identical to the 32-member run after the same steps -- so the
+  parity of the sample holds inside the full batch.
+
+A member's parameters depend on its index only (configs.member_rng), which
+is what makes "member i of the full ensemble" the reference's member i.
+"""
+
+import os
+import zlib
+
+import numpy as np
+import pytest
+
+import paper_2505_17025_b200 as P
+from paper_2505_17025_b200 import _device as D, configs
+from tests.helpers import oracle_depth, rel
+from tests.oracle_cases import GOLDEN
+
+pytestmark = pytest.mark.gpu
+PATH = os.path.join(GOLDEN, "members_full.npz")
+G = np.load(PATH) if os.path.exists(PATH) else None
+HAVE = G is not None and "config4/members" in G.files
+needs_golden = pytest.mark.skipif(not HAVE, reason="members_full.npz (new format) not generated")
+
+
+def _ensemble(cfg, idx):
+    H, Q, W = zip(*(cfg.host_state(int(i), oracle_depth) for i in idx))
+    return P.Ensemble.from_host(cfg.records([int(i) for i in idx]), np.stack(H), np.stack(Q),
+                                np.stack(W))
+
+
+def _crc_counts(bits: np.ndarray, n: int):
+    """[steps][k][nw] uint32 bit-planes -> per-step crc32(packbits(flags)) and counts."""
+    flags = D.bits_to_flags(bits, n)                    # [steps][k][n] bool
+    packed = np.packbits(flags, axis=-1)                # reference's byte order
+    crc = np.array([[zlib.crc32(packed[s, j].tobytes()) for j in range(packed.shape[1])]
+                    for s in range(packed.shape[0])], dtype=np.uint32)
+    return crc, flags.sum(-1)
+
+
+def _check_member(cfg, key, h, hu, t, crc=None, cnt=None):
+    m_time = float(G[key + "/time"])
+    assert t == m_time, (key, t, m_time)
+    i = int(key.split("/")[1])
+    m = cfg.member(i)
+    d = oracle_depth(m.bathymetry, m.grid.sample_nodes, m_time)
+    e_eta, e_hu = rel(h - d, G[key + "/h"] - d), rel(hu, G[key + "/hu"])
+    msg = f"{key}: eta {e_eta:.2e} hu {e_hu:.2e}"
+    if crc is not None:
+        bad = np.flatnonzero(crc != G[key + "/crc"])
+        dc = np.abs(cnt - G[key + "/counts"].astype(np.int64))
+        msg += f", step masks differing {bad.size} (max count diff {dc.max()})"
+        print(msg)
+        assert bad.size == 0, f"{key}: first differing step {bad[:5]}"
+    else:
+        print(msg)
+    assert e_eta <= 1e-9 and e_hu <= 1e-9, msg
+    return e_eta, e_hu
+
+
+@needs_golden
+def test_config4_members_inside_full_ensemble():
+    T = D.torch()
+    cfg = configs.Config4()
+    idx = [int(i) for i in G["config4/members"]]
+    ens = _ensemble(cfg, range(cfg.n_members))   # the reference's own initial states
+    crit = P.Criterion("eta_over_d")
+    N, nw, win = cfg.n_elements, (cfg.n_elements + 31) // 32, 500
+    bits = T.zeros((win, cfg.n_members, nw), dtype=T.int32, device="cuda")
+    sel = T.as_tensor(idx, device="cuda")
+    crcs, cnts = [], []
+    for s0 in range(0, cfg.n_steps, win):
+        k = min(win, cfg.n_steps - s0)
+        bits.zero_()
+        ens.advance(k, "adaptive", crit, flag_bits=bits[:k])
+        sub = bits[:k].index_select(1, sel).cpu().numpy().view(np.uint32)
+        c, n = _crc_counts(sub, N)
+        crcs.append(c)
+        cnts.append(n)
+    st = ens.check()
+    crc, cnt = np.concatenate(crcs), np.concatenate(cnts)
+    h, hu, t = ens.h.cpu().numpy(), ens.hu.cpu().numpy(), ens.time.cpu().numpy()
+    worst = 0.0
+    for j, i in enumerate(idx):
+        e = _check_member(cfg, f"config4/{i}/adaptive", h[i], hu[i], float(t[i]), crc[:, j],
+                          cnt[:, j])
+        worst = max(worst, *e)
+    frac = float(st["flagged"].sum()) / (cfg.n_members * N * cfg.n_steps)
+    print(f"config4 full ensemble: {len(idx)} sampled members, worst {worst:.2e}, "
+          f"ensemble mask fraction {frac:.4f}, max solve residual {st['resid_max'].max():.2e}")
+
+
+@needs_golden
+@pytest.mark.parametrize("mode", ["adaptive", "global"])
+def test_config5_sampled_members_full_length(mode):
+    T = D.torch()
+    cfg = configs.Config5()
+    idx = [int(i) for i in G["config5/members"]]
+    ens = _ensemble(cfg, idx)
+    crit = P.Criterion("eta_over_d") if mode == "adaptive" else None
+    N, nw = cfg.n_elements, (cfg.n_elements + 31) // 32
+    crcs, cnts = [], []
+    win = 2000
+    bits = T.zeros((win, len(idx), nw), dtype=T.int32, device="cuda")
+    for s0 in range(0, cfg.n_steps, win):
+        k = min(win, cfg.n_steps - s0)
+        bits.zero_()
+        ens.advance(k, mode, crit, flag_bits=bits[:k] if mode == "adaptive" else None)
+        if mode == "adaptive":
+            c, n = _crc_counts(bits[:k].cpu().numpy().view(np.uint32), N)
+            crcs.append(c)
+            cnts.append(n)
+    st = ens.check()
+    h, hu, t = ens.h.cpu().numpy(), ens.hu.cpu().numpy(), ens.time.cpu().numpy()
+    worst = 0.0
+    for j, i in enumerate(idx):
+        key = f"config5/{i}/{mode}"
+        if mode == "adaptive":
+            e = _check_member(cfg, key, h[j], hu[j], float(t[j]),
+                              np.concatenate(crcs)[:, j], np.concatenate(cnts)[:, j])
+        else:
+            e = _check_member(cfg, key, h[j], hu[j], float(t[j]))
+        worst = max(worst, *e)
+    print(f"config5 {mode}: {len(idx)} members x {cfg.n_steps} steps, worst {worst:.2e}, "
+          f"max solve residual {st['resid_max'].max():.2e}")
+
+
+@needs_golden
+def test_config5_members_bitwise_inside_full_ensemble():
+    """The sampled members step bit for bit the same inside the 65536-member
+    ensemble (member blocks, kind-ordered grid, shared work lists) as in
+    their own 32-member ensemble."""
+    T = D.torch()
+    cfg = configs.Config5()
+    idx = [int(i) for i in G["config5/members"]]
+    steps = 300
+    crit = P.Criterion("eta_over_d")
+    from bench import init_device
+    sub = cfg.records(idx)
+    small = P.Ensemble(sub, *init_device(cfg, sub, idx))
+    # the device-built initial state (bottom kernel) is the reference's own
+    ref = _ensemble(cfg, idx)
+    for name in ("h", "hu", "hw"):
+        assert T.equal(getattr(small, name), getattr(ref, name)), name
+    small.advance(steps, "adaptive", crit)
+    recs = cfg.records()
+    full = P.Ensemble(recs, *init_device(cfg, recs, list(range(cfg.n_members))))
+    full.advance(steps, "adaptive", crit)
+    T.cuda.synchronize()
+    sel = T.as_tensor(idx, device="cuda")
+    for name in ("h", "hu", "hw", "time"):
+        a = getattr(full, name).index_select(0, sel)
+        b = getattr(small, name)
+        assert T.equal(a, b), name
+    print(f"config5: {len(idx)} members bitwise equal after {steps} steps "
+          f"(full ensemble in blocks of {full.stream_chunk()})")

@@ -13,6 +13,7 @@ import numpy as np
 import pytest
 
 import paper_2505_17025_b200 as P
+from tests.harness import paper_cases
 from paper_2505_17025_b200 import _device as D, configs
 from tests.helpers import oracle_depth, rel
 
@@ -125,7 +126,7 @@ def test_simulate_paper_scenarios_high_order(name):
     device at flat node index e*m + j) against the reference's simulate()."""
     from dataclasses import replace
     c = json.loads(str(GOLD[f"{name}_cfg"]))
-    spec, init = P.build_scenario(c["scenario"], **c["over"])
+    spec, init = paper_cases.build_scenario(c["scenario"], **c["over"])
     spec = replace(spec, gauges=tuple(c["gauges"]))
     crit = P.Criterion(c["kind"], 1e-3, c["enlarge"]) if c["mode"] == "adaptive" else None
     r = P.simulate(spec, init, c["mode"], crit)

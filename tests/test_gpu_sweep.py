@@ -14,8 +14,9 @@ import numpy as np
 import pytest
 
 import paper_2505_17025_b200 as P
+from tests.harness import paper_cases
 from paper_2505_17025_b200 import configs
-from paper_2505_17025_b200.sweep import (criterion_sweep, ensemble_time_ratios, paired_run,
+from tests.harness.sweep import (criterion_sweep, ensemble_time_ratios, paired_run,
                                          write_sweep_csv)
 
 pytestmark = pytest.mark.gpu
@@ -30,7 +31,7 @@ def scenario_from_argv(argv):
     over = {}
     if "--t-end" in a:
         over["t_end"] = float(a["--t-end"])
-    spec, init = P.build_scenario(a["--scenario"], **over)
+    spec, init = paper_cases.build_scenario(a["--scenario"], **over)
     if "--gauges" in a:
         from dataclasses import replace
         spec = replace(spec, gauges=tuple(float(x) for x in a["--gauges"].split(",")))
@@ -70,7 +71,7 @@ def test_sweep_matches_reference_table(name, tmp_path):
 
 
 def test_paired_run_time_ratio():
-    spec, init = P.build_solitary(t_end=5.0)
+    spec, init = paper_cases.build_solitary(t_end=5.0)
     local, glob, ratio = paired_run(spec, init, P.Criterion("eta_over_d", 0.001))
     assert ratio == pytest.approx(local.loop_time / glob.loop_time)
     assert glob.mask_fraction_mean == 1.0 and 0.0 < local.mask_fraction_mean < 1.0

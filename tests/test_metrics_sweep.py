@@ -9,9 +9,9 @@ import os
 import numpy as np
 import pytest
 
-from paper_2505_17025_b200.metrics import (DegenerateSeriesError, RunReport, SeriesPair,
+from tests.harness.metrics import (DegenerateSeriesError, RunReport, SeriesPair,
                                            aligned_pair, pearson, rmse, time_ratio)
-from paper_2505_17025_b200.sweep import SWEEP_HEADER, write_sweep_csv
+from tests.harness.sweep import SWEEP_HEADER, write_sweep_csv
 
 GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "sweep.npz"))
 

@@ -11,6 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2505_17025_b200 as P  # noqa: E402
+from tests.harness import paper_cases
 from paper_2505_17025_b200 import _device as D  # noqa: E402
 
 from paper_2505_17025_b200 import configs  # noqa: E402
@@ -19,7 +20,7 @@ from tests.helpers import oracle_depth  # noqa: E402
 
 def cases():
     for name in ("solitary", "hammack_up", "whittaker"):
-        yield (name,) + P.build_scenario(name) + (("global", "adaptive"),)
+        yield (name,) + paper_cases.build_scenario(name) + (("global", "adaptive"),)
     for name in ("config1", "config2", "config3"):
         cfg = configs.get(name)
         m = cfg.member(0)

@@ -21,8 +21,9 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 import paper_2505_17025_b200 as P  # noqa: E402
+from tests.harness import paper_cases
 from paper_2505_17025_b200 import _device as D, configs  # noqa: E402
-from paper_2505_17025_b200.sweep import criterion_sweep, ensemble_time_ratios  # noqa: E402
+from tests.harness.sweep import criterion_sweep, ensemble_time_ratios  # noqa: E402
 
 
 def table(rows, cols):
@@ -43,7 +44,7 @@ def main():
     cols = ["criterion", "enlarge", "time_ratio", "mask_fraction", "rmse", "r"]
     for name, over, gauges in (("solitary", {}, None),
                                ("hammack_up", {"t_end": 4.0}, (0.61, 1.61, 2.5))):
-        spec, init = P.build_scenario(name, **over)
+        spec, init = paper_cases.build_scenario(name, **over)
         if gauges:
             from dataclasses import replace
             spec = replace(spec, gauges=gauges)
