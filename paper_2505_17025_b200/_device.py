@@ -74,7 +74,8 @@ def member_record(grid, bathy, bcs, dt: float | None, any_order: bool = False) -
         r["mass"] = grid.mass.ravel()
         r["stiffness"] = grid.stiffness.ravel()
         r["deriv_ref"] = grid.deriv_ref.ravel()
-    kind, params = bathy.pack()
+    from .bathymetry import device_model
+    kind, params = device_model(bathy).pack()
     r["bottom_kind"] = kind
     r["bottom"][0, :len(params)] = params
     if bcs is not None:
@@ -153,8 +154,9 @@ def raise_for_status(status: np.ndarray, t0, dt, member: int = 0):
 
 def bottom_sample(model, x: np.ndarray, t: float):
     lib = require_cuda()
+    from .bathymetry import device_model
     rec = np.zeros(1, dtype=_lib.MEMBER_DTYPE)
-    kind, params = model.pack()
+    kind, params = device_model(model).pack()
     rec["bottom_kind"] = kind
     rec["bottom"][0, :len(params)] = params
     m = upload_members(rec)

@@ -196,3 +196,34 @@ def hammack_time_constant(h0: float, b: float, direction: str, g: float = GRAVIT
     if const is None:
         raise ValueError(f"direction must be 'up' or 'down', got {direction!r}")
     return const * b / np.sqrt(g * h0)
+
+
+def device_model(bathy) -> BathymetryModel:
+    """The device form of a bottom model: this package's models as they are,
+    and the reference's own objects (nhswe.FlatBottom, HammackPlate,
+    WhittakerSlide, bathymetry.py:66-184 -- interface sample(x, t), no
+    pack()) mapped by class and fields onto the same device kinds, so a
+    caller can hand reference objects straight to the mirrored API.  Any
+    other model has no device evaluation: TypeError, since the kernels
+    evaluate the bottom analytically in registers."""
+    if hasattr(bathy, "pack"):
+        return bathy
+    kind = type(bathy).__name__
+    try:
+        if kind == "FlatBottom":
+            return FlatBottom(float(bathy.h0))
+        if kind == "HammackPlate":
+            return HammackPlate(float(bathy.h0), float(bathy.zeta0), float(bathy.b),
+                                float(bathy.t_c))
+        if kind == "WhittakerSlide":
+            m = bathy.motion
+            return WhittakerSlide(float(bathy.h0), float(bathy.Hs), float(bathy.Ls),
+                                  SlideMotion(float(m.a0), float(m.u_t), float(m.t1),
+                                              float(m.t2), float(m.t3)),
+                                  float(bathy.x_start))
+    except AttributeError as exc:
+        raise TypeError(f"bottom model {kind}: missing field for its device form ({exc})") from exc
+    raise TypeError(f"bottom model {kind} has no device evaluation: the B200 kernels evaluate "
+                    "FlatBottom, HammackPlate, WhittakerSlide, SmoothBoxPlate and "
+                    "SlopeGaussianSlide analytically; a model known only through sample(x, t) "
+                    "cannot run on the device")

@@ -1,0 +1,72 @@
+"""INTEGRATION.md's reference-side binding (tests/harness/native_stub.py:
+ctypes + the header's structs only) against the library, on the reference's
+own objects: one nh_advance call for a whole simulate loop equals the
+package's resident path bit for bit, and error records map to the
+reference's exceptions."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2505_17025_b200 as P
+from paper_2505_17025_b200 import _lib
+from tests.harness import native_stub as S
+from tests.harness.ref_bridge import import_reference
+
+pytestmark = pytest.mark.gpu
+R, WHERE = import_reference()
+
+
+def test_stub_struct_sizes_match_the_header():
+    assert ctypes.sizeof(S.Member) == _lib.MEMBER_DTYPE.itemsize == 312
+    assert ctypes.sizeof(S.Scheme) == ctypes.sizeof(_lib.Scheme) == 72
+    assert ctypes.sizeof(S.Status) == _lib.STATUS_DTYPE.itemsize == 72
+    lib = S.load()
+    assert lib.nh_abi_version() == _lib.ABI_VERSION
+
+
+@pytest.mark.skipif(R is None, reason=str(WHERE))
+@pytest.mark.parametrize("mode", ["adaptive", "global"])
+def test_stub_simulate_equals_package(mode):
+    lib = S.load()
+    grid = R.GridSpec(0.0, 25.0, 500)
+    bathy = R.HammackPlate(0.05, 0.005, 0.6, 0.13)
+    bcs = R.BoundaryPair(R.WALL, R.ABSORBING)
+    spec = R.ScenarioSpec("plate", grid, 0.01, 1.5, bathy, bcs)
+    d = bathy.sample(grid.sample_nodes, 0.0).d
+    z = np.zeros_like(d)
+    init = R.FlowState(R.NodalField(grid, d), R.NodalField(grid, z), R.NodalField(grid, z), 0.0)
+    crit = R.Criterion("eta_over_d") if mode == "adaptive" else None
+    h, hu, hw, t, st = S.simulate_native(lib, spec, init, mode, crit)
+    S.raise_for(st, 0.0, spec.dt)
+    assert st.steps_done >= 0 and st.resid_max < 1e-12
+    # the package's resident path on the same inputs (its own objects)
+    pg = P.GridSpec(0.0, 25.0, 500)
+    from paper_2505_17025_b200 import _device as D
+    rec = D.member_record(pg, P.HammackPlate(0.05, 0.005, 0.6, 0.13),
+                          P.BoundaryPair(P.WALL, P.ABSORBING), 0.01)
+    ens = P.Ensemble.from_host(rec, d[None], z[None], z[None])
+    ens.advance(spec.n_steps, mode, P.Criterion("eta_over_d") if crit else None, path="resident")
+    ens.check()
+    assert np.array_equal(h, ens.h[0].cpu().numpy())
+    assert np.array_equal(hu, ens.hu[0].cpu().numpy())
+    assert np.array_equal(hw, ens.hw[0].cpu().numpy())
+    assert t == float(ens.time.item())
+
+
+@pytest.mark.skipif(R is None, reason=str(WHERE))
+def test_stub_error_mapping():
+    lib = S.load()
+    grid = R.GridSpec(0.0, 25.0, 200)
+    bathy = R.FlatBottom(0.05)
+    spec = R.ScenarioSpec("dry", grid, 0.01, 0.05, bathy, R.BoundaryPair(R.WALL, R.WALL))
+    h = np.full((200, 2), 0.05)
+    h[50] = -0.01                               # a dry element at entry
+    z = np.zeros_like(h)
+    init = R.FlowState(R.NodalField(grid, h), R.NodalField(grid, z), R.NodalField(grid, z), 0.0)
+    *_, st = S.simulate_native(lib, spec, init, "hydrostatic")
+    from nhswe.hydrostatic import PositivityError
+    with pytest.raises(PositivityError) as ei:
+        S.raise_for(st, 0.0, spec.dt)
+    assert ei.value.element == 50 and ei.value.time == 0.0
