@@ -64,7 +64,10 @@ def test_stub_error_mapping():
     h = np.full((200, 2), 0.05)
     h[50] = -0.01                               # a dry element at entry
     z = np.zeros_like(h)
-    init = R.FlowState(R.NodalField(grid, h), R.NodalField(grid, z), R.NodalField(grid, z), 0.0)
+    # (the reference's FlowState refuses a dry column itself; the raw arrays
+    # reach the device through any object with .h/.hu/.hw.values and .time)
+    from types import SimpleNamespace as NS
+    init = NS(h=NS(values=h), hu=NS(values=z), hw=NS(values=z), time=0.0)
     *_, st = S.simulate_native(lib, spec, init, "hydrostatic")
     from nhswe.hydrostatic import PositivityError
     with pytest.raises(PositivityError) as ei:

@@ -16,7 +16,7 @@ import numpy as np
 import pytest
 
 import paper_2505_17025_b200 as P
-from paper_2505_17025_b200 import configs
+from paper_2505_17025_b200 import _device as D_, configs
 from tests.oracle_cases import GOLDEN, NAMES, load_short
 
 pytestmark = pytest.mark.gpu
@@ -106,44 +106,74 @@ LONG = [(c, m) for c in ("config1", "config2", "config3")
         for m in configs.get(c).modes]
 
 # Config 3's reference solution is dynamically sensitive after the slide stops
-# (t_stop = 1.96 s).  The GPU's solve differs from LAPACK's by ~2e-14 per step
-# (one-step replay), its state drifts to ~1e-10 of the reference by step 20000,
-# and from step 34653 near-threshold mask flips put it on another trajectory.
-# The reference's OWN arithmetic does the same under a perturbation of that
-# size: restarted from its step-20000 checkpoint with h kicked by 1e-10
-# relative (tests/golden/make_config3_kicked.py, config3_kicked.npz) it ends
-# with a full-run mask fraction of 0.555 against its unperturbed 0.465 (the
-# GPU: 0.557).  Exact parity is gated on the reference checkpoints through
-# step 20000 (t = 2.66 s); the full run is compared with the envelope of the
-# reference and its kicked twin.
-CHAOTIC = {"config3": 20000}
+# (t_stop = 1.96 s): a perturbation of the size of one step's solve
+# difference (LAPACK's pivoted band LU vs the condensed chain, ~1e-14) grows
+# until, tens of thousands of steps later, a near-threshold criterion value
+# flips and the run follows another trajectory -- the reference's own
+# arithmetic does the same under a 1e-10 kick (config3_kicked.npz).  Parity
+# over the whole run is therefore checked in WINDOWS: the GPU restarts from
+# every reference checkpoint (make_golden.py saves the state every 5000
+# steps) and must reach the next one within 1e-9 with every per-step mask
+# equal to the reference's.  The free-running full run is compared exactly up
+# to its first flipped mask (test_full_length_config_vs_reference).
+CK_WINDOW = 5000
 
 
-@pytest.mark.parametrize("path", ["resident", "stream"])
-def test_config3_checkpoints_vs_reference(path):
-    """Config 3 against the REAL reference's own states at checkpoint steps
-    (make_golden.py saves them during the full run)."""
+def _config3_windows():
+    path = os.path.join(GOLDEN, "config3_full.npz")
+    if not os.path.exists(path):
+        return []
+    G = np.load(path)
+    cks = sorted(int(k[4:]) for k in G.files if k.startswith("ck/s") and int(k[4:]) % CK_WINDOW == 0)
+    n = int(G["n_steps"])
+    starts = [0] + cks
+    return [(s0, min(s0 + CK_WINDOW, n)) for s0 in starts if s0 < n]
+
+
+def _mask_digests(bits, n):
+    flags = D_.bits_to_flags(bits, n)
+    packed = np.packbits(flags, axis=-1)
+    return (np.array([zlib.crc32(packed[s].tobytes()) for s in range(packed.shape[0])],
+                     dtype=np.uint32), flags.sum(-1))
+
+
+@pytest.mark.parametrize("window", _config3_windows(), ids=lambda w: f"{w[0]}-{w[1]}")
+def test_config3_windows_vs_reference(window):
+    """Config 3 over its whole run, window by window: start at the reference's
+    state of step s0, run to s1; eta / hu within 1e-9 of the reference's state
+    at s1 (its final state for the last window), every step's mask equal."""
+    s0, s1 = window
     G = np.load(os.path.join(GOLDEN, "config3_full.npz"))
-    steps = sorted(int(k[4:]) for k in G.files if k.startswith("ck/s"))
-    if not steps:
-        pytest.skip("config3 checkpoints not generated")
     cfg = configs.config3()
     m = cfg.member(0)
-    ens = P.Ensemble.from_host(cfg.records(), G["h0"][None], G["hu0"][None], G["hw0"][None])
-    done = 0
-    for c in steps:
-        if c > CHAOTIC["config3"]:
-            break
-        ens.advance(c - done, "adaptive", P.Criterion("eta_over_d"), path=path)
-        done = c
-        ens.check()
-        h, hu = ens.h[0].cpu().numpy(), ens.hu[0].cpu().numpy()
-        ref = G[f"ck/s{c}"]
-        assert float(ens.time.item()) == float(G[f"ck/t{c}"])
-        d = m.bathymetry.sample(m.grid.sample_nodes, float(G[f"ck/t{c}"])).d
-        e_eta, e_hu = rel(h - d, ref[0] - d), rel(hu, ref[1])
-        print(f"config3 step {c}: eta {e_eta:.3e} hu {e_hu:.3e}")
-        assert e_eta <= 1e-9 and e_hu <= 1e-9
+    if s0 == 0:
+        st0, t0 = np.stack([G["h0"], G["hu0"], G["hw0"]]), 0.0
+    else:
+        st0, t0 = G[f"ck/s{s0}"], float(G[f"ck/t{s0}"])
+    ens = P.Ensemble.from_host(cfg.records(), st0[0][None], st0[1][None], st0[2][None], [t0])
+    T = D_.torch()
+    n = cfg.n_elements
+    bits = T.zeros((s1 - s0, 1, (n + 31) // 32), dtype=T.int32, device="cuda")
+    ens.advance(s1 - s0, "adaptive", P.Criterion("eta_over_d"), flag_bits=bits)
+    st = ens.check()
+    crc, cnt = _mask_digests(bits.cpu().numpy().view(np.uint32)[:, 0], n)
+    ref_crc, ref_cnt = G["adaptive/flag_crc"][s0:s1], G["adaptive/flag_count"][s0:s1]
+    if s1 == int(G["n_steps"]):
+        ref, t_ref = G["adaptive/final"], None
+    else:
+        ref, t_ref = G[f"ck/s{s1}"], float(G[f"ck/t{s1}"])
+    if t_ref is not None:
+        assert float(ens.time.item()) == t_ref
+    t1 = float(ens.time.item())
+    d = m.bathymetry.sample(m.grid.sample_nodes, t1).d
+    h, hu = ens.h[0].cpu().numpy(), ens.hu[0].cpu().numpy()
+    e_eta, e_hu = rel(h - d, ref[0] - d), rel(hu, ref[1])
+    mism = np.flatnonzero(crc != ref_crc)
+    print(f"config3 steps {s0}-{s1}: eta {e_eta:.2e} hu {e_hu:.2e}, step masks differing "
+          f"{mism.size}, solve residual <= {st['resid_max'][0]:.1e}")
+    assert mism.size == 0, f"first differing steps {(mism[:5] + s0).tolist()}"
+    assert np.array_equal(cnt, ref_cnt)
+    assert e_eta <= 1e-9 and e_hu <= 1e-9
 
 
 @pytest.mark.parametrize("cfg_name,mode", LONG)
@@ -167,20 +197,27 @@ def test_full_length_config_vs_reference(cfg_name, mode):
     e_hu = rel(res.final_state.hu.values, ref[1])
     print(f"{cfg_name} {mode}: eta rel L-inf {e_eta:.3e}, hu rel L-inf {e_hu:.3e}, "
           f"GPU loop {res.loop_time:.3f}s vs reference {float(G[mode + '/loop_time']):.1f}s")
-    if cfg_name in CHAOTIC:
-        assert np.all(np.isfinite(res.final_state.hu.values))
+    if cfg_name == "config3":
+        # free run: exact masks up to the first flip (then the run follows
+        # another trajectory, as the reference's own does under a 1e-10
+        # kick); parity over the whole run is test_config3_windows_vs_reference
         cnt = np.array([sum(e1 - e0 + 1 for e0, e1 in r) for _, _, r in res.mask_history])
-        exact = CHAOTIC[cfg_name]
-        # per-step flagged counts identical to the reference's through the gate
-        assert np.array_equal(cnt[:exact], G[mode + "/flag_count"][:exact])
+        crc = []
+        for _, _, ranges in res.mask_history:
+            f = np.zeros(m.grid.n_elements, bool)
+            for e0, e1 in ranges:
+                f[e0:e1 + 1] = True
+            crc.append(zlib.crc32(np.packbits(f).tobytes()))
+        mism = np.flatnonzero(np.array(crc, dtype=np.uint32) != G[mode + "/flag_crc"])
+        first = int(mism[0]) if mism.size else n_steps
         K = np.load(os.path.join(GOLDEN, f"{cfg_name}_kicked.npz"))
-        lo = min(float(G[mode + "/mask_fraction"]), float(K["mask_fraction"]))
-        hi = max(float(G[mode + "/mask_fraction"]), float(K["mask_fraction"]))
-        print(f"{cfg_name}: mask fraction GPU {res.mask_fraction_mean:.4f}, reference "
+        print(f"{cfg_name} free run: masks identical to the reference for steps 0..{first - 1} "
+              f"of {n_steps}; mask fraction GPU {res.mask_fraction_mean:.4f}, reference "
               f"{float(G[mode + '/mask_fraction']):.4f}, reference kicked by "
               f"{float(K['rel']):.0e} at step {int(K['start'])}: {float(K['mask_fraction']):.4f}")
-        assert lo - 0.02 <= res.mask_fraction_mean <= hi + 0.02
-        assert np.abs(eta).max() < 2 * np.abs(eta_ref).max()
+        assert first > 30000   # past the slide's stop (step ~14740), well into the wave phase
+        assert np.array_equal(cnt[:first], G[mode + "/flag_count"][:first])
+        assert np.all(np.isfinite(res.final_state.hu.values))
         return
     assert e_eta <= 1e-9 and e_hu <= 1e-9
     if mode == "adaptive":
