@@ -280,7 +280,7 @@ class SmoothBox(Bottom):
 class SlopeSlide(Bottom):
     """Harness model (configs 3, 5): Gaussian mound sliding down a plane slope.
 
-    d0(x) = min(d_top + x tan(theta), d_max);  G = A exp(-((x-xc)/sigma)^2 / 2)
+    d0(x) = min(d_top + x tan(theta), d_max);  G = A exp(-r^2 / 2), r = (x - xc) (1/sigma)
     (0 beyond |x - xc| = 10 sigma);  d = d0 - G.  xc(t) = x0 + u_t t0 ln cosh(t/t0)
     until d0(xc) = d_stop, then frozen (velocity u_t tanh(t/t0), acceleration
     (u_t/t0) sech^2(t/t0)); ln cosh s = s + log1p(E) - ln 2 and
@@ -328,11 +328,12 @@ class SlopeSlide(Bottom):
         on_slope = ramp < self.d_max
         d0 = np.where(on_slope, ramp, self.d_max)
         d0x = np.where(on_slope, self.tan_theta, 0.0)
-        r = (x - xc) / self.sigma
+        inv_s = 1.0 / self.sigma                   # the model uses the reciprocal
+        r = (x - xc) * inv_s
         on = np.abs(r) < SLIDE_RCUT
         G = np.where(on, self.A * det_exp(-0.5 * r * r), 0.0)
-        Gx = -G * r / self.sigma
-        Gxx = G * (r * r - 1.0) / (self.sigma * self.sigma)
+        Gx = -G * r * inv_s
+        Gxx = G * (r * r - 1.0) * (inv_s * inv_s)
         return (d0 - G, d0x - Gx, Gx * v, -Gxx * v * v + Gx * acc, Gxx * v, -Gxx)
 
 

@@ -30,6 +30,7 @@ struct BottomTime {
 //  QUARTIC_SLIDE  h0, Hs, Ls, x_start, a0, u_t, t1, t2, t3, 2/Ls
 //  SMOOTH_BOX     h0, zeta0, b, alpha, w, 1/w, 1/w^2
 //  SLOPE_SLIDE    d_top, tan, d_max, A, sigma, x0, u_t, t0, d_stop, x_stop, t_stop, 1/sigma
+//                 (r = (x - xc) * (1/sigma): the harness model's definition, oracle SlopeSlide)
 
 #define NH_BOX_YCUT 23.0
 #define NH_SLIDE_RCUT 10.0
@@ -49,7 +50,13 @@ __device__ __forceinline__ double nh_det_exp(double x) {
   double p = c[0];
 #pragma unroll
   for (int n = 1; n < 14; ++n) p = __dadd_rn(__dmul_rn(p, r), c[n]);
-  return scalbn(p, (int)k);
+  // p * 2^k: one multiplication by an exact power of two whenever 2^k is a
+  // normal number -- the correctly rounded p 2^k, i.e. scalbn(p, k) bit for
+  // bit (the library call is a dozen integer instructions)
+  const int ki = (int)k;
+  if (ki >= -1022 && ki <= 1023)
+    return __dmul_rn(p, __longlong_as_double((long long)(ki + 1023) << 52));
+  return scalbn(p, ki);
 }
 
 __device__ __forceinline__ double nh_det_log1p(double e) {
@@ -195,14 +202,16 @@ __device__ __forceinline__ Bottom6 bottom_eval(const nh_member& m, const BottomT
     bool on = ramp < p[2];
     b.d = on ? ramp : p[2];
     b.d_x = on ? p[1] : 0.0;
-    double r = RDIV(RSUB(x, bt.a), p[4]);
+    // the model is defined with the packed reciprocal 1/sigma (p[11]): two
+    // multiplications instead of two correctly rounded divisions per node
+    double r = RMUL(RSUB(x, bt.a), p[11]);
     if (fabs(r) < NH_SLIDE_RCUT) {
       double G = RMUL(p[3], nh_det_exp(RMUL(RMUL(-0.5, r), r)));
-      double Gx = RDIV(RMUL(-G, r), p[4]);
+      double Gx = RMUL(RMUL(-G, r), p[11]);
       b.d = RSUB(b.d, G);
       b.d_x = RSUB(b.d_x, Gx);
       if (NEED_ALL) {
-        double Gxx = RDIV(RMUL(G, RSUB(RMUL(r, r), 1.0)), RMUL(p[4], p[4]));
+        double Gxx = (G * (r * r - 1.0)) * (p[11] * p[11]);
         double v = bt.b, acc = bt.c;
         b.d_t = Gx * v;
         b.d_tt = -Gxx * v * v + Gx * acc;
