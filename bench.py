@@ -230,7 +230,7 @@ def _cpu_worker(args):
 
             def step(s):
                 r = O.step(mem, s[0], s[1], s[2], s[3], mode)
-                return (r.h, r.hu, r.hw, r.time)
+                return (r.h, r.hu, r.hw, s[3] + m.dt)
         for _ in range(spin):
             st = step(st)
         t0 = time.perf_counter()
@@ -398,7 +398,7 @@ def run_b200(args):
 
     # end to end through the public API: the post-warm-up state in pinned
     # HOST memory -> driver.advance_host (member blocks: copy-in, K steps,
-    # copy-out, pipelined on three streams) -> host; wall clock around
+    # copy-out, pipelined on three streams over three device buffers) -> host; wall clock around
     # synchronizes, max over ranks
     e2e = {"skipped": e2e_note} if e2e_note else None
     if host0 is not None:
@@ -415,7 +415,7 @@ def run_b200(args):
                "d2h_bytes_per_step": nbytes / args.steps,
                "ms": ems, "block_members": args.e2e_block,
                "call": "driver.advance_host(pinned host h, hu, hw, time; K steps): member blocks "
-                       "copied in, stepped and copied out, pipelined on 3 CUDA streams; from the "
+                       "copied in, stepped and copied out, pipelined on 3 CUDA streams and 3 device buffers (both copy directions overlap the compute); from the "
                        "post-warm-up state (the K steps of region 1)"}
         del host0
 
@@ -489,7 +489,7 @@ def main():
     ap.add_argument("--global-steps", type=int, default=10)
     ap.add_argument("--cpu-steps", type=int, default=200)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
-    ap.add_argument("--e2e-block", type=int, default=4096)
+    ap.add_argument("--e2e-block", type=int, default=2048)
     ap.add_argument("--kernel-steps", type=int, default=0,
                     help="steps of timed region 2 (per-kernel events); default: --steps")
     args = ap.parse_args()

@@ -190,8 +190,9 @@ def advance_host(records: np.ndarray, h, hu, hw, time, n_steps: int, mode: str =
     h, hu, hw: CPU float64 tensors (B, N, 2) -- pinned memory gives
     asynchronous copies; time: CPU float64 (B,).  The members are streamed
     through the GPU in blocks of `block` members, pipelined on three CUDA
-    streams: the copy-in of block i+1 and the copy-out of block i-1 overlap
-    the K steps of block i (two device buffers, one streaming workspace).
+    streams: the copy-in of block i+1 and the copy-out of block i-1 both
+    overlap the K steps of block i (three device buffers, so the two copy
+    directions run at the same time; one streaming workspace).
     This is the end-to-end call for ensembles kept on the host (the bench's
     e2e leg); members are independent, so the result equals
     Ensemble(...).advance(n_steps) bit for bit.  Returns the nh_status
@@ -208,20 +209,21 @@ def advance_host(records: np.ndarray, h, hu, hw, time, n_steps: int, mode: str =
         raise ValueError("h, hu, hw must be (B, N, 2) P1 states of equal shape")
     c = criterion if criterion is not None else Criterion("eta_over_d")
     sch = D.scheme(_MODES[mode], c.kind, c.k_nh, c.enlarge, flux, g, rho)
-    block = max(1, min(B, block or 4096))
+    block = max(1, min(B, block or 2048))
+    NBUF = 3   # block i computes while block i+1 copies in and block i-1 copies out
     members = D.upload_members(np.ascontiguousarray(records))
     status = D.new_status(B)
     rec, stb = _lib.MEMBER_DTYPE.itemsize, _lib.STATUS_DTYPE.itemsize
     ws = D.stream_workspace(block, N)
     bufs = [[T.empty((block, N, 2), dtype=T.float64, device="cuda") for _ in range(3)] +
-            [T.empty(block, dtype=T.float64, device="cuda")] for _ in range(2)]
+            [T.empty(block, dtype=T.float64, device="cuda")] for _ in range(NBUF)]
     host = (h, hu, hw, time)
     s_in, s_cmp, s_out = T.cuda.Stream(), T.cuda.current_stream(), T.cuda.Stream()
     s_in.wait_stream(s_cmp)
-    freed = [None, None]       # event: the buffer's previous copy-out finished
+    freed = [None] * NBUF      # event: the buffer's previous copy-out finished
     for i, c0 in enumerate(range(0, B, block)):
         c1 = min(B, c0 + block)
-        n, k = c1 - c0, i & 1
+        n, k = c1 - c0, i % NBUF
         buf = bufs[k]
         with T.cuda.stream(s_in):
             if freed[k] is not None:
