@@ -39,14 +39,28 @@ struct BottomTime {
 // det_log1p): IEEE +,-,* only -- Cody-Waite reduction and Horner polynomials,
 // explicit round-to-nearest intrinsics (never contracted), same constants and
 // order as the numpy definition, so host and device round identically.
+#if NH_OPT_EXPC
+// the Horner coefficients as constant-bank operands of the DADDs (as
+// immediates every coefficient costs two uniform-register moves)
+static __constant__ double NH_EXP_COEF[14] = {
+    1.6059043836821613e-10, 2.08767569878681e-09, 2.505210838544172e-08,
+    2.755731922398589e-07,  2.7557319223985893e-06, 2.48015873015873e-05,
+    0.0001984126984126984,  0.001388888888888889, 0.008333333333333333,
+    0.041666666666666664,   0.16666666666666666, 0.5, 1.0, 1.0};
+#endif
+
 __device__ __forceinline__ double nh_det_exp(double x) {
   const double k = rint(__dmul_rn(x, 1.4426950408889634));
   const double r = __dsub_rn(__dsub_rn(x, __dmul_rn(k, 0.6931471803691238)),
                              __dmul_rn(k, 1.9082149292705877e-10));
+#if NH_OPT_EXPC
+  const double* c = NH_EXP_COEF;
+#else
   const double c[14] = {1.6059043836821613e-10, 2.08767569878681e-09, 2.505210838544172e-08,
                         2.755731922398589e-07,  2.7557319223985893e-06, 2.48015873015873e-05,
                         0.0001984126984126984,  0.001388888888888889, 0.008333333333333333,
                         0.041666666666666664,   0.16666666666666666, 0.5, 1.0, 1.0};
+#endif
   double p = c[0];
 #pragma unroll
   for (int n = 1; n < 14; ++n) p = __dadd_rn(__dmul_rn(p, r), c[n]);
@@ -57,6 +71,40 @@ __device__ __forceinline__ double nh_det_exp(double x) {
   if (ki >= -1022 && ki <= 1023)
     return __dmul_rn(p, __longlong_as_double((long long)(ki + 1023) << 52));
   return scalbn(p, ki);
+}
+
+// Two arguments at once: the same operations per argument as nh_det_exp (so
+// the same bits), the two Horner chains interleaved in one basic block -- a
+// single chain is 26 dependent fp64 operations.
+__device__ __forceinline__ void nh_det_exp2(double xa, double xb, double& ya, double& yb) {
+  const double ka = rint(__dmul_rn(xa, 1.4426950408889634));
+  const double kb = rint(__dmul_rn(xb, 1.4426950408889634));
+  const double ra = __dsub_rn(__dsub_rn(xa, __dmul_rn(ka, 0.6931471803691238)),
+                              __dmul_rn(ka, 1.9082149292705877e-10));
+  const double rb = __dsub_rn(__dsub_rn(xb, __dmul_rn(kb, 0.6931471803691238)),
+                              __dmul_rn(kb, 1.9082149292705877e-10));
+#if NH_OPT_EXPC
+  const double* c = NH_EXP_COEF;
+#else
+  const double c[14] = {1.6059043836821613e-10, 2.08767569878681e-09, 2.505210838544172e-08,
+                        2.755731922398589e-07,  2.7557319223985893e-06, 2.48015873015873e-05,
+                        0.0001984126984126984,  0.001388888888888889, 0.008333333333333333,
+                        0.041666666666666664,   0.16666666666666666, 0.5, 1.0, 1.0};
+#endif
+  double pa = c[0], pb = c[0];
+#pragma unroll
+  for (int n = 1; n < 14; ++n) {
+    pa = __dadd_rn(__dmul_rn(pa, ra), c[n]);
+    pb = __dadd_rn(__dmul_rn(pb, rb), c[n]);
+  }
+  const int ia = (int)ka, ib = (int)kb;
+  if (ia >= -1022 && ia <= 1023 && ib >= -1022 && ib <= 1023) {
+    ya = __dmul_rn(pa, __longlong_as_double((long long)(ia + 1023) << 52));
+    yb = __dmul_rn(pb, __longlong_as_double((long long)(ib + 1023) << 52));
+  } else {
+    ya = scalbn(pa, ia);
+    yb = scalbn(pb, ib);
+  }
 }
 
 __device__ __forceinline__ double nh_det_log1p(double e) {
@@ -266,6 +314,44 @@ __device__ __forceinline__ Bottom6 bottom_eval_sp(const nh_member& m, const Bott
     return b;
   }
   return bottom_eval<KIND, false>(m, bt, x);
+}
+
+// d and d_x at both nodes of an element (predictor stages): bit-identical to
+// two bottom_eval_sp calls; the slope slide's two Gaussians share one
+// branch so their exp chains interleave (nh_det_exp2).
+template <int KIND>
+__device__ __forceinline__ void bottom_eval_sp2(const nh_member& m, const BottomTime& bt,
+                                                double x0, double x1, const BottomSpace& s0,
+                                                const BottomSpace& s1, Bottom6& b0, Bottom6& b1) {
+#if NH_OPT_EXP2
+  if (KIND == NH_BOTTOM_SLOPE_SLIDE) {
+    const double* p = m.bottom;
+    const double ramp0 = RADD(p[0], RMUL(x0, p[1])), ramp1 = RADD(p[0], RMUL(x1, p[1]));
+    const bool on0 = ramp0 < p[2], on1 = ramp1 < p[2];
+    b0 = Bottom6{on0 ? ramp0 : p[2], on0 ? p[1] : 0.0, 0.0, 0.0, 0.0, 0.0};
+    b1 = Bottom6{on1 ? ramp1 : p[2], on1 ? p[1] : 0.0, 0.0, 0.0, 0.0, 0.0};
+    const double r0 = RMUL(RSUB(x0, bt.a), p[11]), r1 = RMUL(RSUB(x1, bt.a), p[11]);
+    const bool g0 = fabs(r0) < NH_SLIDE_RCUT, g1 = fabs(r1) < NH_SLIDE_RCUT;
+    if (g0 || g1) {
+      // a node outside the cut-off evaluates exp(0) and discards it
+      double E0, E1;
+      nh_det_exp2(g0 ? RMUL(RMUL(-0.5, r0), r0) : 0.0, g1 ? RMUL(RMUL(-0.5, r1), r1) : 0.0, E0, E1);
+      if (g0) {
+        const double G = RMUL(p[3], E0), Gx = RMUL(RMUL(-G, r0), p[11]);
+        b0.d = RSUB(b0.d, G);
+        b0.d_x = RSUB(b0.d_x, Gx);
+      }
+      if (g1) {
+        const double G = RMUL(p[3], E1), Gx = RMUL(RMUL(-G, r1), p[11]);
+        b1.d = RSUB(b1.d, G);
+        b1.d_x = RSUB(b1.d_x, Gx);
+      }
+    }
+    return;
+  }
+#endif
+  b0 = bottom_eval_sp<KIND>(m, bt, x0, s0);
+  b1 = bottom_eval_sp<KIND>(m, bt, x1, s1);
 }
 
 // KIND = -1: run-time dispatch on m.bottom_kind (CTA-uniform in the

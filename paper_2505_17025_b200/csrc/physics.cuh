@@ -83,9 +83,9 @@ NH_DEV Face face_flux(const Side& L, const Side& R, double g, double& speed) {
   if (LEVEL) {
     hLs = L.h; hRs = R.h;
   } else {
-    double dm = fmin(L.d, R.d);
-    hLs = fmax(RSUB(L.h, RSUB(L.d, dm)), 0.0);
-    hRs = fmax(RSUB(R.h, RSUB(R.d, dm)), 0.0);
+    double dm = nh_min(L.d, R.d);
+    hLs = nh_max(RSUB(L.h, RSUB(L.d, dm)), 0.0);
+    hRs = nh_max(RSUB(R.h, RSUB(R.d, dm)), 0.0);
     cL = RMUL(hg, RSUB(RMUL(L.h, L.h), RMUL(hLs, hLs)));
     cR = RMUL(hg, RSUB(RMUL(R.h, R.h), RMUL(hRs, hRs)));
   }
@@ -104,7 +104,7 @@ NH_DEV Face face_flux(const Side& L, const Side& R, double g, double& speed) {
   }
   double aL = RADD(fabs(L.u), sL);
   double aR = RADD(fabs(R.u), sR);
-  speed = fmax(aL, aR);
+  speed = nh_max(aL, aR);
   double lam = RMUL(0.5, speed);
   double qL = RMUL(hLs, L.u), qR = RMUL(hRs, R.u);
   Face f;

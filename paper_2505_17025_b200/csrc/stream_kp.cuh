@@ -32,8 +32,13 @@ __device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q
                                            const BottomSpace& s0, const BottomSpace& s1, int i,
                                            int e, int N, double* sh, double* sf, double t6[6],
                                            double& speed, double& d0, double& d1) {
-  Bottom6 b0 = bottom_eval_sp_k<KIND>(m, bt, x0, s0);
-  Bottom6 b1 = bottom_eval_sp_k<KIND>(m, bt, x1, s1);
+  Bottom6 b0, b1;
+  if (KIND >= 0) {
+    bottom_eval_sp2<KIND>(m, bt, x0, x1, s0, s1, b0, b1);
+  } else {
+    b0 = bottom_eval_sp_k<KIND>(m, bt, x0, s0);
+    b1 = bottom_eval_sp_k<KIND>(m, bt, x1, s1);
+  }
   Side n0, n1;
   make_sides_warp(q.h0, q.q0, q.w0, b0.d, q.h1, q.q1, q.w1, b1.d, n0, n1);
   sh[0 * TPB + i] = q.h1; sh[1 * TPB + i] = q.q1; sh[2 * TPB + i] = q.w1; sh[3 * TPB + i] = b1.d;
@@ -54,13 +59,13 @@ __device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q
   }
   double sp;
   Face fl = face_flux<KIND == NH_BOTTOM_FLAT, true>(L, n0, g, sp);
-  speed = fmax(speed, sp);
+  speed = nh_max(speed, sp);
   sf[0 * TPB + i] = fl.F1; sf[1 * TPB + i] = fl.F2L; sf[2 * TPB + i] = fl.F3;
   __syncthreads();
   Face fr;
   if (e == N - 1) {
     fr = face_flux<KIND == NH_BOTTOM_FLAT>(n1, ghost_side(n1, m.bc_right), g, sp);
-    speed = fmax(speed, sp);
+    speed = nh_max(speed, sp);
   } else {
     int k = i < TPB - 1 ? i + 1 : i;
     fr.F1 = sf[0 * TPB + k]; fr.F2L = sf[1 * TPB + k]; fr.F3 = sf[2 * TPB + k]; fr.F2R = 0.0;
@@ -316,11 +321,28 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   if (sch.mode == NH_MODE_ADAPTIVE && sch.criterion == NH_CRIT_ETA_OVER_D) {
     // the default criterion, evaluated by the whole warp (one vote for both
     // divisions); halo slots past the domain ends compute and discard
-    bool badc = false;
     const double e0 = RSUB(qp.h0, d0), e1 = RSUB(qp.h1, d1);
+#if NH_OPT_CRIT
+    // |e / d| > k decided without the division wherever that is certain:
+    // with p = k d, |e| >= p (1 + 2^-50) puts e / d more than an ulp above k
+    // and |e| <= p (1 - 2^-50) more than an ulp below it, so the rounded
+    // quotient compares the same way.  Only an element inside that 2^-49
+    // band takes the correctly rounded division (one warp vote) -- the flag
+    // is the reference's bit for bit.
+    const double k = sch.k_nh;
+    const double a0 = fabs(e0), a1 = fabs(e1), p0 = k * d0, p1 = k * d1;
+    const double up = 1.0 + 0x1p-50, dn = 1.0 - 0x1p-50;
+    const bool sure = a0 >= p0 * up || a1 >= p1 * up;
+    const bool amb = !sure && (a0 > p0 * dn || a1 > p1 * dn);
+    bool hit = sure;
+    NH_WARP_FIX(amb, (hit = sure || nh_max(fabs(RDIVP(e0, d0)), fabs(RDIVP(e1, d1))) > k));
+    raw = (valid && hit) ? 1 : 0;
+#else
+    bool badc = false;
     double v0 = fabs(nh_div_pos_fp(e0, d0, badc)), v1 = fabs(nh_div_pos_fp(e1, d1, badc));
     NH_WARP_FIX(badc, (v0 = fabs(RDIVP(e0, d0)), v1 = fabs(RDIVP(e1, d1))));
-    raw = (valid && fmax(v0, v1) > sch.k_nh) ? 1 : 0;
+    raw = (valid && nh_max(v0, v1) > sch.k_nh) ? 1 : 0;
+#endif
   } else
 #endif
   if (valid && sch.mode != NH_MODE_HYDROSTATIC) {
@@ -355,7 +377,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
           break;
         }
       }
-      raw = fmax(v0, v1) > sch.k_nh ? 1 : 0;
+      raw = nh_max(v0, v1) > sch.k_nh ? 1 : 0;
     }
   }
   rf[i] = raw;
@@ -494,6 +516,10 @@ __device__ __forceinline__ void kp_correct_and_step(const StreamArgs& a, const T
   if (a.hw_any) {   // w / w_x criterion: member-wide any(hw != 0) of the step input
     if (__syncthreads_or(ti.own && (q.w0 != 0.0 || q.w1 != 0.0)) && i == 0) a.hw_any[b] = 1;
   }
+#ifdef NH_KP_ONLY_KIND   // diagnostics: one body, for reading its SASS (cuobjdump) in isolation
+  kp_body<NH_KP_ONLY_KIND, FUSE>(a, msh, mc, ti, q, ks, sq);
+  return;
+#endif
   switch (msh.bottom_kind) {
     case NH_BOTTOM_FLAT: kp_body<NH_BOTTOM_FLAT, FUSE>(a, msh, mc, ti, q, ks, sq); break;
     case NH_BOTTOM_PLATE: kp_body<NH_BOTTOM_PLATE, FUSE>(a, msh, mc, ti, q, ks, sq); break;

@@ -1,7 +1,10 @@
 """DRAM traffic per launch of one kernel from an `ncu --set full` report ->
 profiles/kp_traffic.json (read by bench.py for roofline.traffic).
 
-usage: python tools/ncu_traffic.py rep.ncu-rep kernel_regex out.json
+usage: python tools/ncu_traffic.py rep.ncu-rep kernel_regex out.json [workload cells_per_launch]
+
+bench.py reads profiles/kp_traffic_<workload>.json: dram_bytes_per_cell scales
+the capture (a 4096-member probe, tools/kp_probe.py) to the launch it times.
 """
 import csv
 import io
@@ -11,7 +14,7 @@ import subprocess
 import sys
 
 
-def main(rep, pattern, out):
+def main(rep, pattern, out, workload="config4", cells=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -37,15 +40,18 @@ def main(rep, pattern, out):
                                             "nan").replace(",", "")),
         })
     r0 = recs[0]
-    res = {"source": rep.split("/")[-1], "workload": "config4", "kernel": r0["kernel"], "grid": r0["grid"],
+    res = {"source": rep.split("/")[-1], "workload": workload, "kernel": r0["kernel"], "grid": r0["grid"],
            "block": r0["block"],
            "dram_bytes_per_launch": r0["dram_read_bytes"] + r0["dram_write_bytes"],
            "dram_read_bytes": r0["dram_read_bytes"], "dram_write_bytes": r0["dram_write_bytes"],
            "ncu_duration_ms": r0["duration_ms"], "launches_captured": len(recs),
            "fp64_pipe_active_pct": r0["fp64_pipe_pct"], "issue_active_pct": r0["issue_active_pct"]}
+    if cells:
+        res["cells_per_launch"] = int(cells)
+        res["dram_bytes_per_cell"] = res["dram_bytes_per_launch"] / int(cells)
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:6])
