@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define NH_ABI_VERSION 4   /* 2: nh_outputs gauge fields; 3: nh_pm_* (orders p > 1), w / w_x on nh_stream_advance;
+#define NH_ABI_VERSION 5   /* 5: nh_pm_ldg_solve takes outer_left and residual_tol (general LDG flux); 2: nh_outputs gauge fields; 3: nh_pm_* (orders p > 1), w / w_x on nh_stream_advance;
                                4: residual gate (nh_scheme.residual_tol, nh_status resid_*) */
 
 /* bottom model kinds (reference bathymetry.py:66-184 + harness models) */
@@ -222,10 +222,13 @@ typedef struct nh_pm_member {
 size_t nh_pm_workspace_bytes(int m, int n_members, int n_elements);
 
 /* nh_advance for m nodes per element (modes HYDROSTATIC / GLOBAL / ADAPTIVE,
- * every criterion, alternating LDG flux; outputs flag_bits, p_nh [B][N][m],
- * gauges with flat node index e*m + j).  Per step: two Heun-stage kernels,
- * then flags, per-element LDG condensation, one chain thread per member,
- * reconstruction and the hw correction. */
+ * every criterion, any LDG flux; outputs flag_bits, p_nh [B][N][m], gauges
+ * with flat node index e*m + j).  Per step: two Heun-stage kernels, then
+ * flags, per-element LDG condensation, one chain thread per member,
+ * reconstruction and the hw correction; with a flux outside the alternating
+ * family the condensation / chain / reconstruction are replaced by one band
+ * solve per range (see nh_pm_ldg_solve).  This is also the P1 (m = 2) path
+ * for such a flux. */
 int nh_pm_advance(const nh_member* members, const nh_pm_member* pm, int m,
                   int n_members, int n_elements, double* h, double* hu, double* hw,
                   double* time, int n_steps, const nh_scheme* scheme,
@@ -249,7 +252,16 @@ int nh_pm_criterion(const nh_member* members, const nh_pm_member* pm, int m, int
  *  nh_pm_ldg_solve        ldg_solve / solve_on_ranges (corrector.py:292-424) on
  *                         the flagged ranges (flags [B][ceil(N/32)]),
  *                         outer_right [B][N] = hu right of each element;
- *                         writes p (0 off the ranges) and hu on the ranges;
+ *                         writes p (0 off the ranges) and hu on the ranges.
+ *                         Any FluxCoefficients (corrector.py:40-47): the
+ *                         alternating family (c12 = -1/2, c22 = 0) runs the
+ *                         condensed chain; any other flux assembles each
+ *                         range's band system as the reference does and
+ *                         solves it by band elimination with partial
+ *                         pivoting (what dgbsv does, corrector.py:352), with
+ *                         the residual gate (residual_tol > 0).  That path
+ *                         also needs outer_left [B][N] = hu left of each
+ *                         element (NULL otherwise: its weight is 0);
  *  nh_pm_correct_momentum correct_momentum (corrector.py:427-482): hw_out =
  *                         hw + dt/rho * bottom pressure on the flagged elements. */
 int nh_pm_coefficients(const nh_member* members, const nh_pm_member* pm, int m, int n_members,
@@ -257,9 +269,9 @@ int nh_pm_coefficients(const nh_member* members, const nh_pm_member* pm, int m, 
                        const double* time, double g, double rho, double* coef, void* stream);
 int nh_pm_ldg_solve(const nh_member* members, const nh_pm_member* pm, int m, int n_members,
                     int n_elements, const double* coef, const uint32_t* flags,
-                    const double* outer_right, double rho, double c11, double c12, double c22,
-                    double* p, double* hu, nh_status* status, void* workspace,
-                    size_t workspace_bytes, void* stream);
+                    const double* outer_left, const double* outer_right, double rho, double c11,
+                    double c12, double c22, double residual_tol, double* p, double* hu,
+                    nh_status* status, void* workspace, size_t workspace_bytes, void* stream);
 int nh_pm_correct_momentum(const nh_member* members, const nh_pm_member* pm, int m,
                            int n_members, int n_elements, const double* h, const double* p,
                            const double* coef, const uint32_t* flags, double rho,

@@ -100,6 +100,20 @@ def pm_record(grid) -> np.ndarray:
     return r
 
 
+def pm_from_members(records: np.ndarray) -> np.ndarray:
+    """nh_pm_member records of P1 members from their nh_member records (the
+    same operators, m = 2): the m-node kernels then run a P1 ensemble -- the
+    path of an LDG flux outside the alternating family."""
+    records = np.atleast_1d(records)
+    r = np.zeros(len(records), dtype=_lib.PM_DTYPE)
+    for f in ("weak_div", "mass", "stiffness", "deriv_ref"):
+        r[f][:, :4] = records[f].reshape(len(records), 4)
+    r["lift_left"][:, :2] = records["lift_left"].reshape(len(records), 2)
+    r["lift_right"][:, :2] = records["lift_right"].reshape(len(records), 2)
+    r["node_off"][:, 1] = records["dx"].reshape(len(records))
+    return r
+
+
 def upload_members(records: np.ndarray):
     """Structured member table -> device byte tensor."""
     raw = np.ascontiguousarray(records).view(np.uint8)

@@ -59,7 +59,7 @@ class Outputs(ctypes.Structure):
                 ("gauge_h", ctypes.c_void_p), ("n_gauges", ctypes.c_int32)]
 
 
-ABI_VERSION = 4   # include/nhswe_b200.h NH_ABI_VERSION
+ABI_VERSION = 5   # include/nhswe_b200.h NH_ABI_VERSION
 
 EXPORTS = ("nh_abi_version", "nh_advance", "nh_stream_advance", "nh_stream_workspace_bytes",
            "nh_rhs", "nh_criterion", "nh_coefficients",
@@ -99,7 +99,7 @@ _SIGS = {
     "nh_pm_rhs": ([_P, _P, _I, _I, _I, _P, _P, _P, _P, _D, _P, _P, _P, _P, _P], _I),
     "nh_pm_criterion": ([_P, _P, _I, _I, _I, _P, _P, _P, _P, _I, _P, _P], _I),
     "nh_pm_coefficients": ([_P, _P, _I, _I, _I, _P, _P, _P, _P, _D, _D, _P, _P], _I),
-    "nh_pm_ldg_solve": ([_P, _P, _I, _I, _I, _P, _P, _P, _D, _D, _D, _D, _P, _P, _P, _P,
+    "nh_pm_ldg_solve": ([_P, _P, _I, _I, _I, _P, _P, _P, _P, _D, _D, _D, _D, _D, _P, _P, _P, _P,
                          ctypes.c_size_t, _P], _I),
     "nh_pm_correct_momentum": ([_P, _P, _I, _I, _I, _P, _P, _P, _P, _D, _P, _P, _P], _I),
 }

@@ -10,10 +10,13 @@ Every function keeps the reference signature and runs on the GPU:
   "correct given flags" mode (coefficients, solve and momentum update in one
   launch, corrector.py:485-498).
 
-The GPU solve supports the reference's alternating flux family
-(c12 = -1/2, c22 = 0, any c11) -- the only one the reference ever uses; other
-flux constants raise ``ValueError`` before any work is done.  Every solve
-carries the reference's residual gate (corrector.py:355-366): the relative
+The condensed chain solve serves the reference's alternating flux family
+(c12 = -1/2, c22 = 0, any c11), its default and the one every config uses.
+Any other ``FluxCoefficients`` runs the general path of the m-node kernels
+(``nh_pm_ldg_solve`` / ``nh_pm_advance``): each range's band system assembled
+as the reference assembles it and solved by band elimination with partial
+pivoting, what ``dgbsv`` does (a coverage path, one thread per member).  Every
+solve carries the reference's residual gate (corrector.py:355-366): the relative
 residual of the batched system is evaluated on the device and above
 ``residual_tol`` raises ``EllipticSolveError``.  Adjacent ranges are separate
 systems, as in the reference's block-diagonal batch.
@@ -125,11 +128,9 @@ def assemble_coefficients(predictor: FlowState, bathy: BathymetryModel, dt: floa
     return EllipticCoefficients(grid, s11, s12, -s11, s22, f1, f2, phi, full, dt, rho, off)
 
 
-def _check_flux(flux: FluxCoefficients):
-    if flux.c12 != -0.5 or flux.c22 != 0.0:
-        raise ValueError(
-            f"unsupported LDG flux {flux}: the B200 solve condenses the system for the "
-            "alternating flux family c12 = -1/2, c22 = 0 (any c11), the reference default")
+def is_alternating(flux: FluxCoefficients | None) -> bool:
+    """The flux family of the condensed chain solve (c12 = -1/2, c22 = 0)."""
+    return flux is None or (flux.c12 == -0.5 and flux.c22 == 0.0)
 
 
 def _has_adjacent(ranges) -> bool:
@@ -137,10 +138,16 @@ def _has_adjacent(ranges) -> bool:
 
 
 def _solve_device(coeffs: EllipticCoefficients, ranges, outer_right: np.ndarray,
-                  flux: FluxCoefficients, residual_tol: float = 1e-10):
-    """Run nh_ldg_solve; returns full-grid (p, hu) host arrays (hu only valid on ranges)."""
+                  flux: FluxCoefficients, residual_tol: float = 1e-10,
+                  outer_left: np.ndarray | None = None):
+    """Run nh_ldg_solve; returns full-grid (p, hu) host arrays (hu only valid on ranges).
+
+    outer_left [n]: hu left of each element -- only a flux outside the
+    alternating family gives it a weight (0.5 + c12, corrector.py:346)."""
     lib = D.require_cuda()
-    _check_flux(flux)
+    general = not is_alternating(flux)
+    if general and outer_left is None:
+        raise ValueError("a general LDG flux needs the left outer traces")
     grid = coeffs.grid
     n = grid.n_elements
     off = coeffs.offset
@@ -150,18 +157,19 @@ def _solve_device(coeffs: EllipticCoefficients, ranges, outer_right: np.ndarray,
         if e0 - off < 0 or e1 - off >= len(coeffs.s11):
             raise ValueError(f"range {(e0, e1)} outside the coefficient window")
     nodes = grid.poly_order + 1
-    if nodes != 2 and _has_adjacent(ranges):
-        # the m-node chain has no range-start input: solve every other range
+    pm = nodes != 2 or general   # the m-node kernels (also P1 with a general flux)
+    if pm and _has_adjacent(ranges):
+        # the m-node solves have no range-start input: solve every other range
         # per call, so no two ranges of a call touch
-        p, hu = _solve_device(coeffs, ranges[0::2], outer_right, flux, residual_tol)
-        p2, hu2 = _solve_device(coeffs, ranges[1::2], outer_right, flux, residual_tol)
+        p, hu = _solve_device(coeffs, ranges[0::2], outer_right, flux, residual_tol, outer_left)
+        p2, hu2 = _solve_device(coeffs, ranges[1::2], outer_right, flux, residual_tol, outer_left)
         for e0, e1 in ranges[1::2]:
             p[e0:e1 + 1], hu[e0:e1 + 1] = p2[e0:e1 + 1], hu2[e0:e1 + 1]
         return p, hu
     planes = np.zeros((7, 1, n, nodes))
     sl = slice(off, off + len(coeffs.s11))
     fields = (coeffs.s11, coeffs.s12, coeffs.s22, coeffs.f1, coeffs.f2)
-    if nodes != 2:   # the m-node solve stores phi / d_x with its element blocks
+    if pm:   # the m-node solve stores phi / d_x with its element blocks
         fields += (coeffs.phi, coeffs.bottom.d_x)
     for i, arr in enumerate(fields):
         planes[i, 0, sl] = arr
@@ -176,17 +184,19 @@ def _solve_device(coeffs: EllipticCoefficients, ranges, outer_right: np.ndarray,
     fb = D.dev(D.flags_to_bits(flags[None]).view(np.int32), dtype=np.int32)
     sb = D.dev(D.flags_to_bits(starts[None]).view(np.int32), dtype=np.int32)
     orr = D.dev(outer_right[None])
+    orl = D.dev(np.asarray(outer_left, dtype=np.float64)[None]) if general else None
     T = D.torch()
     p = T.zeros((1, n, nodes), dtype=T.float64, device="cuda")
     hu = T.zeros((1, n, nodes), dtype=T.float64, device="cuda")
     st = D.new_status(1)
-    if nodes != 2:
+    if pm:
         ws = D.pm_workspace(nodes, 1, n)
         _lib.check(lib.nh_pm_ldg_solve(D.ptr(m), D.ptr(D.upload_members(D.pm_record(grid))),
-                                       nodes, 1, n, D.ptr(cp), D.ptr(fb), D.ptr(orr),
-                                       coeffs.rho, flux.c11, flux.c12, flux.c22, D.ptr(p),
-                                       D.ptr(hu), D.ptr(st), D.ptr(ws), ws.numel(),
-                                       D.stream_ptr()), "nh_pm_ldg_solve")
+                                       nodes, 1, n, D.ptr(cp), D.ptr(fb), D.ptr(orl), D.ptr(orr),
+                                       coeffs.rho, flux.c11, flux.c12, flux.c22,
+                                       float(residual_tol), D.ptr(p), D.ptr(hu), D.ptr(st),
+                                       D.ptr(ws), ws.numel(), D.stream_ptr()),
+                   "nh_pm_ldg_solve")
     else:
         _lib.check(lib.nh_ldg_solve(D.ptr(m), 1, n, D.ptr(cp), D.ptr(fb), D.ptr(sb), D.ptr(orr),
                                     coeffs.rho, flux.c11, flux.c12, flux.c22,
@@ -212,7 +222,8 @@ def ldg_solve(coeffs: EllipticCoefficients, elements: tuple[int, int],
     e0, e1 = (int(v) for v in elements)
     n = coeffs.grid.n_elements
     outer = np.full(n, float(outer_hu[1]))
-    p, hu = _solve_device(coeffs, ((e0, e1),), outer, flux, residual_tol)
+    p, hu = _solve_device(coeffs, ((e0, e1),), outer, flux, residual_tol,
+                          np.full(n, float(outer_hu[0])))
     return p[e0:e1 + 1].copy(), hu[e0:e1 + 1].copy()
 
 
@@ -226,13 +237,23 @@ def _outer_right(predictor: FlowState, bcs: BoundaryPair) -> np.ndarray:
     return out
 
 
+def _outer_left(predictor: FlowState, bcs: BoundaryPair) -> np.ndarray:
+    """Outer hu trace left of each element (corrector.py:388-403)."""
+    hu = predictor.hu.values
+    out = np.empty(hu.shape[0])
+    out[1:] = hu[:-1, -1]
+    out[0] = bcs.left.ghost(predictor.h.values[0, 0], hu[0, 0], predictor.hw.values[0, 0])[1]
+    return out
+
+
 def solve_on_ranges(predictor: FlowState, coeffs: EllipticCoefficients, ranges,
                     bcs: BoundaryPair,
                     flux: FluxCoefficients = FluxCoefficients()) -> PressureSolution:
     """Independent per-range solves (corrector.py:406-424)."""
     grid = predictor.grid
     ranges = tuple(sorted(tuple(int(v) for v in r) for r in ranges))
-    p, hu = _solve_device(coeffs, ranges, _outer_right(predictor, bcs), flux)
+    p, hu = _solve_device(coeffs, ranges, _outer_right(predictor, bcs), flux,
+                          outer_left=None if is_alternating(flux) else _outer_left(predictor, bcs))
     p_full = np.zeros_like(predictor.h.values)
     hu_full = predictor.hu.values.copy()
     for e0, e1 in ranges:
@@ -289,13 +310,12 @@ def apply_correction(predictor: FlowState, bathy: BathymetryModel, dt: float, ra
                      ) -> tuple[FlowState, PressureSolution]:
     """Full correction on the flagged ranges, one fused launch (corrector.py:485-498)."""
     D.require_cuda()
-    _check_flux(flux)
     grid = predictor.grid
     n = grid.n_elements
     ranges = tuple(sorted(tuple(int(v) for v in r) for r in ranges))
     if not ranges:
         raise ValueError("apply_correction needs at least one range")
-    if _has_adjacent(ranges):
+    if _has_adjacent(ranges) or not is_alternating(flux):
         # adjacent ranges are separate systems: the reference's own pipeline
         # (corrector.py:485-498) of the three device kernels, whose solve
         # splits the flagged run at the given range starts

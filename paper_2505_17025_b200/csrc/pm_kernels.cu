@@ -66,8 +66,11 @@ struct PmArgs {
   const uint32_t* given;   // NH_MODE_CORRECT_GIVEN: [B][ceil(N/32)] ranges to correct
   const double* coef;      // coefficient-level calls: [7][B*N*M] s11 s12 s22 f1 f2 phi d_x
   const double* outer_right;   // coefficient-level solve: [B][N] hu right of each element
+  const double* outer_left;    // ... and left of each element (general flux only)
+  double* gen;      // general-flux band solve scratch, gen_doubles(M, N) per member
   int step;
   int corr;         // the step has a correction (mode != hydrostatic)
+  int general;      // LDG flux outside the alternating family: pm_general_solve
   nh_scheme sch;
   int B, N;
 };
@@ -540,7 +543,7 @@ __global__ void __launch_bounds__(PTB) pm_chain(PmArgs a) {
   const int N = a.N;
   const size_t BN = (size_t)a.B * N, base = (size_t)b * N;
   const nh_member& m = a.members[b];
-  if (a.corr) {
+  if (a.corr && !a.general) {
     double s = 0.0, t = 0.0;   // a_{-1} = 0: the left outer trace has zero weight
     for (int e = 0; e < N; ++e) {
       const size_t k = base + e;
@@ -570,6 +573,226 @@ __global__ void __launch_bounds__(PTB) pm_chain(PmArgs a) {
   a.time[b] = a.time[b] + m.dt;   // t + dt per step (hydrostatic.py:206-209)
   a.status[b].steps_done += 1;
   if (a.hw_any) a.hw_any[b] = 0;
+}
+
+// ------------------------------------------------------ general LDG flux
+// Any FluxCoefficients (corrector.py:40-47).  Outside the alternating family
+// (c12 = -1/2, c22 = 0) an element couples to both neighbours through P and Q
+// at both faces, so the two-scalar chain above does not apply.  This coverage
+// path does what the reference does (corrector.py:173-234 pattern, :329-349
+// values, :352 dgbsv): every range's node-interleaved band system is
+// assembled in LAPACK general-band storage and solved by Gaussian
+// elimination with partial pivoting (kl = ku = 2m - 1), one thread per
+// member, its ranges in turn; the residual gate (corrector.py:359-366) is
+// evaluated on the saved matrix.  Scratch per member (gen_doubles):
+//   ab [3 band + 1][2 m N]  factorisation, column-major like dgbsv's work array
+//   am [2 band + 1][2 m N]  the matrix as assembled (residual)
+//   bx [2 m N]              right-hand side -> solution;  b0 [2 m N]  its copy
+template <int M>
+__host__ __device__ constexpr size_t gen_doubles(size_t N) {
+  return (size_t)(3 * (2 * M - 1) + 1 + 2 * (2 * M - 1) + 1 + 2) * 2 * M * N;
+}
+
+template <int M>
+__global__ void __launch_bounds__(PTB) pm_general_solve(PmArgs a) {
+  const int b = blockIdx.x * PTB + threadIdx.x;
+  if (b >= a.B) return;
+  constexpr int BAND = 2 * M - 1, LDAB = 3 * BAND + 1, LDAM = 2 * BAND + 1;
+  const int N = a.N;
+  const size_t BN = (size_t)a.B * N, BNM = BN * M, base = (size_t)b * N;
+  const nh_member& m = a.members[b];
+  const nh_pm_member& c = a.pm[b];
+  const double rho = a.sch.rho, inv_rho = 1.0 / rho;
+  const double c11 = a.sch.c11, c12 = a.sch.c12, c22 = a.sch.c22;
+  double* ab = a.gen + (size_t)b * gen_doubles<M>(N);
+  double* am = ab + (size_t)LDAB * 2 * M * N;
+  double* bx = am + (size_t)LDAM * 2 * M * N;
+  double* b0 = bx + (size_t)2 * M * N;
+  const LdgConst lk = make_ldg_const(m.dt, a.sch.g, rho);
+  BottomTime bt1{0.0, 0.0, 0.0};
+  if (!a.coef) bt1 = bottom_time(m, a.given ? a.time[b] : a.time[b] + m.dt);
+  auto flagged = [&](int e) -> bool {
+    return a.coef ? given_flag(a, b, e) : a.flags[base + e] != 0;
+  };
+  double r2 = 0.0, b2 = 0.0, x2 = 0.0, amax = 0.0;
+  bool solved = false;
+  int e = 0;
+  while (e < N) {
+    if (!flagged(e)) {
+      if (a.p)
+        for (int j = 0; j < M; ++j) a.p[(base + e) * M + j] = 0.0;
+      ++e;
+      continue;
+    }
+    const int e0 = e;
+    while (e < N && flagged(e)) ++e;
+    const int e1 = e - 1, n = e1 - e0 + 1, size = 2 * M * n;
+    // outer hu traces of the range (corrector.py:388-403), read before the
+    // range's own hu is replaced
+    double outer_l, outer_r;
+    if (a.coef) {
+      outer_l = a.outer_left ? a.outer_left[base + e0] : 0.0;
+      outer_r = a.outer_right[base + e1];
+    } else {
+      if (e0 > 0) {
+        outer_l = a.hu_out[(base + e0 - 1) * M + M - 1];
+      } else {
+        const double q0 = a.hu_out[base * M];
+        outer_l = m.bc_left == NH_BC_WALL ? -q0 : q0;
+      }
+      if (e1 < N - 1) {
+        outer_r = a.hu_out[(base + e1 + 1) * M];
+      } else {
+        const double qn = a.hu_out[(base + N - 1) * M + M - 1];
+        outer_r = m.bc_right == NH_BC_WALL ? -qn : qn;
+      }
+    }
+    for (size_t k = 0; k < (size_t)LDAB * size; ++k) ab[k] = 0.0;
+    for (size_t k = 0; k < (size_t)LDAM * size; ++k) am[k] = 0.0;
+    auto add = [&](int r, int cc, double v) {
+      ab[(size_t)cc * LDAB + (2 * BAND + r - cc)] += v;
+      am[(size_t)cc * LDAM + (BAND + r - cc)] += v;
+    };
+    for (int k = 0; k < n; ++k) {
+      const size_t idx = base + e0 + k, o = idx * M;
+      NodeCoef nc[M];
+      double dxb[M];
+      if (a.coef) {
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          nc[j].s11 = a.coef[o + j];
+          nc[j].s12 = a.coef[BNM + o + j];
+          nc[j].s22 = a.coef[2 * BNM + o + j];
+          nc[j].f1 = a.coef[3 * BNM + o + j];
+          nc[j].f2 = a.coef[4 * BNM + o + j];
+        }
+      } else {
+        const Elem<M> q = load_elem<M>(a.h_out, a.hu_out, a.hw_out, o);
+        element_coefficients<M>(m, c, bt1, lk, q, e0 + k, nc, dxb);
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          a.pdx[(size_t)j * BN + idx] = nc[j].phi;
+          a.pdx[(size_t)(M + j) * BN + idx] = dxb[j];
+        }
+        bool ok = true;
+#pragma unroll
+        for (int j = 0; j < M; ++j) ok = ok && !(nc[j].s12 <= 0.0);
+        if (!ok) nh_report(a.status + b, a.step, NH_ERR_STRUCTURE, e0 + k);
+      }
+      const int r0 = 2 * M * k;
+      double f1[M], f2[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) { f1[j] = nc[j].f1 * inv_rho; f2[j] = nc[j].f2; }
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          const double Mij = c.mass[i * M + j], Kij = c.stiffness[i * M + j];
+          add(r0 + 2 * i, r0 + 2 * j, -Kij + Mij * nc[j].s11);
+          add(r0 + 2 * i, r0 + 2 * j + 1, Mij * (nc[j].s12 * inv_rho));
+          add(r0 + 2 * i + 1, r0 + 2 * j + 1, -Kij + Mij * (-nc[j].s11));
+          add(r0 + 2 * i + 1, r0 + 2 * j, Mij * (rho * nc[j].s22));
+        }
+        bx[r0 + 2 * i] = rowdot<M>(f1, c.mass, i);
+        bx[r0 + 2 * i + 1] = rowdot<M>(f2, c.mass, i);
+      }
+      if (k + 1 < n) {   // interior face k | k + 1 (corrector.py:205-224)
+        const int pL = r0 + 2 * (M - 1), qL = pL + 1, pR = r0 + 2 * M, qR = pR + 1;
+        const int cols[4] = {pL, pR, qL, qR};
+        const double sp[4] = {0.5 - c12, 0.5 + c12, c22, -c22};   // p* weights
+        const double sq[4] = {c11, -c11, 0.5 + c12, 0.5 - c12};   // hu* weights
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if (sp[t] != 0.0) { add(pL, cols[t], sp[t]); add(pR, cols[t], -sp[t]); }
+          if (sq[t] != 0.0) { add(qL, cols[t], sq[t]); add(qR, cols[t], -sq[t]); }
+        }
+      }
+    }
+    // range ends: p* = 0; hu* keeps its interior-trace terms, the outer
+    // traces go to the right-hand side (corrector.py:226-231, :346-347)
+    add(1, 1, -(0.5 - c12));
+    add(1, 0, c11);
+    add(size - 1, size - 1, 0.5 + c12);
+    add(size - 1, size - 2, c11);
+    bx[1] += (0.5 + c12) * outer_l;
+    bx[size - 1] -= (0.5 - c12) * outer_r;
+    for (int k = 0; k < size; ++k) b0[k] = bx[k];
+    // band LU with partial pivoting, the right-hand side carried along
+    bool ok = true;
+    int ju = 0;
+    for (int j = 0; j < size; ++j) {
+      double* col = ab + (size_t)j * LDAB + 2 * BAND;   // A(j + i, j) = col[i]
+      const int km = min(BAND, size - 1 - j);
+      int jp = 0;
+      double best = fabs(col[0]);
+      for (int i = 1; i <= km; ++i)
+        if (fabs(col[i]) > best) { best = fabs(col[i]); jp = i; }
+      if (!(best > 0.0) || !isfinite(best)) { ok = false; break; }
+      ju = max(ju, min(j + BAND + jp, size - 1));
+      if (jp) {
+        for (int cc = j; cc <= ju; ++cc) {
+          double* p0 = ab + (size_t)cc * LDAB + (2 * BAND + j - cc);
+          const double tmp = p0[0]; p0[0] = p0[jp]; p0[jp] = tmp;
+        }
+        const double tb = bx[j]; bx[j] = bx[j + jp]; bx[j + jp] = tb;
+      }
+      const double rp = 1.0 / col[0];
+      for (int i = 1; i <= km; ++i) {
+        const double l = col[i] * rp;
+        if (l == 0.0) continue;
+        for (int cc = j + 1; cc <= ju; ++cc) {
+          double* pc = ab + (size_t)cc * LDAB + (2 * BAND + j - cc);
+          pc[i] = fma(-l, pc[0], pc[i]);
+        }
+        bx[j + i] = fma(-l, bx[j], bx[j + i]);
+      }
+    }
+    if (ok) {
+      for (int j = size - 1; j >= 0; --j) {
+        double v = bx[j];
+        const int cmax = min(size - 1, j + 2 * BAND);
+        for (int cc = j + 1; cc <= cmax; ++cc)
+          v = fma(-ab[(size_t)cc * LDAB + (2 * BAND + j - cc)], bx[cc], v);
+        bx[j] = v / ab[(size_t)j * LDAB + 2 * BAND];
+      }
+    } else {
+      nh_report(a.status + b, a.step, NH_ERR_SOLVE_PIVOT, e0);
+    }
+    // residual shares of this range (the reference's norms run over the
+    // whole batched system of the step)
+    bool fin = true;
+    for (int r = 0; r < size; ++r) {
+      double v = -b0[r];
+      const int clo = max(0, r - BAND), chi = min(size - 1, r + BAND);
+      for (int cc = clo; cc <= chi; ++cc) {
+        const double av = am[(size_t)cc * LDAM + (BAND + r - cc)];
+        v = fma(av, bx[cc], v);
+        amax = fmax(amax, fabs(av));
+      }
+      r2 += v * v;
+      b2 += b0[r] * b0[r];
+      x2 += bx[r] * bx[r];
+      fin = fin && isfinite(bx[r]);
+    }
+    solved = true;
+    if (ok && !fin) nh_report(a.status + b, a.step, NH_ERR_SOLVE_NONFINITE, e0);
+    for (int k = 0; k < n; ++k) {
+      const size_t o = (base + e0 + k) * M;
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        a.p[o + j] = rho * bx[2 * (M * k + j)];   // p = rho P (corrector.py:368)
+        a.hu_out[o + j] = bx[2 * (M * k + j) + 1];
+      }
+    }
+  }
+  if (solved) {
+    nh_status* st = a.status + b;
+    const double scale = fmax(fmax(sqrt(b2), amax * sqrt(x2)), 1e-300);
+    const double rel = sqrt(r2) / scale;
+    if (rel > st->resid_max) st->resid_max = rel;
+    if (a.sch.residual_tol > 0.0 && rel > a.sch.residual_tol)
+      nh_report(st, a.step, NH_ERR_SOLVE_RESIDUAL, -1);
+  }
 }
 
 // ----------------------------------------------------------- reconstruction
@@ -716,9 +939,13 @@ int pm_advance_m(PmArgs a, int n_steps, double** A, double** Bb, const nh_output
     a.h_in = a.h_out = A[0]; a.hu_in = a.hu_out = A[1]; a.hw_in = a.hw_out = A[2];
     a.step = 0;
     int rc = launch((void*)pm_flags, BN, args, s);
-    if (!rc) rc = launch((void*)pm_condense<M>, BN, args, s);
-    if (!rc) rc = launch((void*)pm_chain<M>, a.B, args, s);
-    if (!rc) rc = launch((void*)pm_reconstruct<M>, BN, args, s);
+    if (a.general) {
+      if (!rc) rc = launch((void*)pm_general_solve<M>, a.B, args, s);
+    } else {
+      if (!rc) rc = launch((void*)pm_condense<M>, BN, args, s);
+      if (!rc) rc = launch((void*)pm_chain<M>, a.B, args, s);
+      if (!rc) rc = launch((void*)pm_reconstruct<M>, BN, args, s);
+    }
     if (!rc) rc = launch((void*)pm_correct<M>, BN, args, s);
     if (!rc && out && out->p_nh &&
         cudaMemcpyAsync(out->p_nh, a.p, (size_t)BN * M * 8, cudaMemcpyDeviceToDevice, s) !=
@@ -735,9 +962,10 @@ int pm_advance_m(PmArgs a, int n_steps, double** A, double** Bb, const nh_output
     int rc = launch((void*)pm_stage<M, 1>, BN, args, s);
     if (!rc) rc = launch((void*)pm_stage<M, 2>, BN, args, s);
     if (!rc && a.corr) rc = launch((void*)pm_flags, BN, args, s);
-    if (!rc && a.corr) rc = launch((void*)pm_condense<M>, BN, args, s);
-    if (!rc) rc = launch((void*)pm_chain<M>, a.B, args, s);
-    if (!rc && a.corr) rc = launch((void*)pm_reconstruct<M>, BN, args, s);
+    if (!rc && a.corr && a.general) rc = launch((void*)pm_general_solve<M>, a.B, args, s);
+    if (!rc && a.corr && !a.general) rc = launch((void*)pm_condense<M>, BN, args, s);
+    if (!rc) rc = launch((void*)pm_chain<M>, a.B, args, s);   // (general: time advance only)
+    if (!rc && a.corr && !a.general) rc = launch((void*)pm_reconstruct<M>, BN, args, s);
     if (!rc && a.corr) rc = launch((void*)pm_correct<M>, BN, args, s);
     if (!rc && a.n_gauges > 0) rc = launch((void*)pm_gauges<M>, a.B * a.n_gauges, args, s);
     if (rc) return rc;
@@ -778,6 +1006,12 @@ double* carve(PmArgs& a, void* workspace, int m, int B, int N, int*& hw_any) {
 template <class F>
 void* by_m(int m, F f2, F f3, F f4) { return m == 2 ? f2 : m == 3 ? f3 : f4; }
 
+size_t gen_doubles_m(int m, size_t N) {
+  return m == 2 ? gen_doubles<2>(N) : m == 3 ? gen_doubles<3>(N) : gen_doubles<4>(N);
+}
+
+bool alternating(double c12, double c22) { return c12 == -0.5 && c22 == 0.0; }
+
 }  // namespace
 
 extern "C" {
@@ -800,7 +1034,6 @@ int nh_pm_advance(const nh_member* members, const nh_pm_member* pm, int m, int B
   if (sc.mode < NH_MODE_HYDROSTATIC || sc.mode > NH_MODE_CORRECT_GIVEN) return NH_E_UNSUPPORTED;
   if (sc.mode == NH_MODE_CORRECT_GIVEN && (!outputs || !outputs->given_flags || n_steps != 1))
     return NH_E_ARG;
-  if (sc.mode != NH_MODE_HYDROSTATIC && (sc.c12 != -0.5 || sc.c22 != 0.0)) return NH_E_UNSUPPORTED;
   if (n_steps == 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t BN = (size_t)B * N, BNM = BN * m;
@@ -808,6 +1041,16 @@ int nh_pm_advance(const nh_member* members, const nh_pm_member* pm, int m, int B
   std::memset(&a, 0, sizeof a);
   int* hw_any = nullptr;
   double* alt = carve(a, workspace, m, B, N, hw_any);
+  // a flux outside the alternating family: band solve per range (pm_general_solve)
+  a.general = sc.mode != NH_MODE_HYDROSTATIC && !alternating(sc.c12, sc.c22);
+  void* gen = nullptr;
+  if (a.general) {
+    if (cudaMallocAsync(&gen, gen_doubles_m(m, N) * (size_t)B * 8, s) != cudaSuccess) {
+      cudaGetLastError();
+      return NH_E_CUDA;
+    }
+    a.gen = (double*)gen;
+  }
   const bool wcrit = sc.mode == NH_MODE_ADAPTIVE &&
                      (sc.criterion == NH_CRIT_W || sc.criterion == NH_CRIT_W_X);
   if (cudaMemsetAsync(a.raw, 0, BN, s) != cudaSuccess) return NH_E_CUDA;
@@ -825,11 +1068,14 @@ int nh_pm_advance(const nh_member* members, const nh_pm_member* pm, int m, int B
   a.sch = sc; a.B = B; a.N = N;
   double* A[3] = {h, hu, hw};
   double* Bb[3] = {alt, alt + BNM, alt + 2 * BNM};
+  int rc;
   switch (m) {
-    case 2: return pm_advance_m<2>(a, n_steps, A, Bb, outputs, s);
-    case 3: return pm_advance_m<3>(a, n_steps, A, Bb, outputs, s);
-    default: return pm_advance_m<4>(a, n_steps, A, Bb, outputs, s);
+    case 2: rc = pm_advance_m<2>(a, n_steps, A, Bb, outputs, s); break;
+    case 3: rc = pm_advance_m<3>(a, n_steps, A, Bb, outputs, s); break;
+    default: rc = pm_advance_m<4>(a, n_steps, A, Bb, outputs, s); break;
   }
+  if (gen) cudaFreeAsync(gen, s);
+  return rc;
 }
 
 int nh_pm_rhs(const nh_member* members, const nh_pm_member* pm, int m, int B, int N,
@@ -880,15 +1126,37 @@ int nh_pm_coefficients(const nh_member* members, const nh_pm_member* pm, int m, 
 }
 
 int nh_pm_ldg_solve(const nh_member* members, const nh_pm_member* pm, int m, int B, int N,
-                    const double* coef, const uint32_t* flags, const double* outer_right,
-                    double rho, double c11, double c12, double c22, double* p, double* hu,
-                    nh_status* status, void* workspace, size_t workspace_bytes, void* stream) {
+                    const double* coef, const uint32_t* flags, const double* outer_left,
+                    const double* outer_right, double rho, double c11, double c12, double c22,
+                    double residual_tol, double* p, double* hu, nh_status* status,
+                    void* workspace, size_t workspace_bytes, void* stream) {
   if (!members || !pm || !coef || !flags || !outer_right || !p || !hu || !status || !workspace)
     return NH_E_ARG;
   if (m < 2 || m > NH_PM_MAX_NODES || B < 1 || N < 2) return NH_E_ARG;
   if (workspace_bytes < nh_pm_workspace_bytes(m, B, N)) return NH_E_ARG;
-  if (c12 != -0.5 || c22 != 0.0) return NH_E_UNSUPPORTED;
   cudaStream_t s = (cudaStream_t)stream;
+  if (!alternating(c12, c22)) {   // general flux: one band solve per range
+    if (!outer_left) return NH_E_ARG;
+    PmArgs g;
+    std::memset(&g, 0, sizeof g);
+    g.members = members; g.pm = pm; g.status = status; g.B = B; g.N = N;
+    g.coef = coef; g.given = flags; g.outer_left = outer_left; g.outer_right = outer_right;
+    g.corr = 1; g.general = 1;
+    g.sch.rho = rho; g.sch.c11 = c11; g.sch.c12 = c12; g.sch.c22 = c22;
+    g.sch.residual_tol = residual_tol;
+    g.hu_out = hu; g.p = p;
+    void* gen = nullptr;
+    if (cudaMallocAsync(&gen, gen_doubles_m(m, N) * (size_t)B * 8, s) != cudaSuccess) {
+      cudaGetLastError();
+      return NH_E_CUDA;
+    }
+    g.gen = (double*)gen;
+    void* gargs[1] = {&g};
+    const int rc = launch(by_m(m, (void*)pm_general_solve<2>, (void*)pm_general_solve<3>,
+                               (void*)pm_general_solve<4>), B, gargs, s);
+    cudaFreeAsync(gen, s);
+    return rc;
+  }
   PmArgs a;
   std::memset(&a, 0, sizeof a);
   int* hw_any = nullptr;

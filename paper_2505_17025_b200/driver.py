@@ -139,6 +139,12 @@ class Ensemble:
         sch = D.scheme(_MODES[mode], c.kind, c.k_nh, c.enlarge, flux, g, rho)
         if path == "auto":
             path = self.choose_path(mode, criterion)
+        if mode != "hydrostatic" and (flux.c12 != -0.5 or flux.c22 != 0.0):
+            # an LDG flux outside the alternating family: the m-node kernels'
+            # band solve per range (P1 members: operators from their records)
+            path = "generic"
+            if self.pm is None and self.M == 2:
+                self.pm = D.upload_members(D.pm_from_members(self.records))
         if self.M != 2 or path == "generic":   # m-node kernels (orders p > 1)
             if self.pm is None:
                 raise ValueError("path='generic' needs pm_records")

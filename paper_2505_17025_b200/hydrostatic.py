@@ -103,8 +103,12 @@ def _advance_one(state: FlowState, dt: float, bathy, bcs, mode: int, g: float, r
     """One fused step of a single member; returns host arrays + flags/p/status."""
     grid = state.grid
     T = D.torch()
-    pm = grid.poly_order != 1
-    m = D.upload_members(D.member_record(grid, bathy, bcs, dt, any_order=pm))
+    # orders p > 1, and P1 with an LDG flux outside the alternating family,
+    # run the m-node kernels (csrc/pm_kernels.cu)
+    general = (mode != _lib.MODE_HYDROSTATIC and flux is not None
+               and (flux.c12 != -0.5 or flux.c22 != 0.0))
+    pm = grid.poly_order != 1 or general
+    m = D.upload_members(D.member_record(grid, bathy, bcs, dt, any_order=grid.poly_order != 1))
     h, hu, hw = _upload_state(state)
     t = D.dev(np.array([state.time]))
     st = D.new_status(1)
@@ -113,7 +117,7 @@ def _advance_one(state: FlowState, dt: float, bathy, bcs, mode: int, g: float, r
     p = T.zeros_like(h) if want_p else None
     gv = D.dev(np.asarray(given, np.uint32).view(np.int32), dtype=np.int32) if given is not None else None
     sch = D.scheme(mode, kind, k_nh, enlarge, flux, g, rho)
-    if pm:   # orders p > 1: the m-node kernels (csrc/pm_kernels.cu)
+    if pm:
         D.pm_advance(m, D.upload_members(D.pm_record(grid)), h, hu, hw, t, 1, sch, st, fb, p,
                      given=gv)
     else:

@@ -10,8 +10,8 @@ reference's behaviour on the same inputs (tests/golden/errors.npz, made by
 * touching ranges are separate systems (each with P* = 0 at its ends, the
   reference's block-diagonal batch): apply_correction / solve_on_ranges on
   ((2, n/4), (n/4+1, n/2), ...) match the reference;
-* a non-alternating flux is rejected with ValueError (the reference solves it;
-  the condensed chain is built for c12 = -1/2, c22 = 0).
+* a flux outside the alternating family is solved, as in the reference, by
+  the band solve of the m-node kernels, with the same residual gate.
 """
 
 import os
@@ -120,10 +120,15 @@ def test_structural_asserts_match_reference():
         P.ldg_solve(co, (3, 40))
 
 
-def test_unsupported_flux_is_a_value_error():
-    assert str(E["err/flux_c12_0"]) == "ok"   # the reference solves it
-    with pytest.raises(ValueError, match="flux"):
-        P.ldg_solve(_coeffs(), (3, 40), flux=P.FluxCoefficients(0.5, 0.0, 0.0))
+def test_general_flux_is_solved_and_gated():
+    """A flux outside the alternating family: the reference solves it, and so
+    does the band solve of the m-node kernels (values: tests/test_gpu_flux.py),
+    with the same residual gate."""
+    assert str(E["err/flux_c12_0"]) == "ok"
+    central = P.FluxCoefficients(0.5, 0.0, 0.0)
+    assert _outcome(lambda: P.ldg_solve(_coeffs(), (3, 40), (0.2, 0.3), central)) == "ok"
+    with pytest.raises(P.EllipticSolveError, match="residual"):
+        P.ldg_solve(_coeffs(), (3, 40), (0.2, 0.3), central, residual_tol=1e-18)
 
 
 @pytest.mark.parametrize("name", ["flat_walls", "flat_absorbing", "plate"])
