@@ -555,8 +555,14 @@ int nh_stream_advance(const nh_member* members, int B, int N, double* h, double*
     a.pend = pend[(n_steps - 1) & 1];
     a.flags_prev = flags[(n_steps - 1) & 1];
     a.finalize = 1;
+    a.tile_count = tcount + ((n_steps - 1) & 1);   // the last step's list of flagged tiles
     void* args[1] = {&a};
-    if (int rc = stream_launch(kp, 4, gp, bpp, args, s, kp_smem)) return rc;
+    static const bool fin_list = !getenv("NH_KFIN_LIST") || atoi(getenv("NH_KFIN_LIST")) != 0;
+    if (fin_list) {
+      if (int rc = stream_launch(nh_stream_kfin_ptr(), 4, gc, bpp, args, s, kp_smem)) return rc;
+    } else if (int rc = stream_launch(kp, 4, gp, bpp, args, s, kp_smem)) {
+      return rc;
+    }
   }
   if (cur) {
     for (int f = 0; f < 3; ++f)

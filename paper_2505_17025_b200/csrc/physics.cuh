@@ -348,7 +348,7 @@ NH_DEV void ldg_residual(const nh_member& m, const NodeCoef& c0, const NodeCoef&
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       v = fma(A[i][j], x[j], v);
-      amax = fmax(amax, fabs(A[i][j]));
+      amax = nh_max(amax, fabs(A[i][j]));
     }
     res[i] = v;
   }
@@ -359,11 +359,11 @@ NH_DEV void ldg_residual(const nh_member& m, const NodeCoef& c0, const NodeCoef&
   res[1] -= c11 * a_prev;
   res[3] += z_next;
   double b3 = range_end ? r[3] - z_next : r[3];
-  if (!range_start || !range_end) amax = fmax(amax, fmax(1.0, fabs(c11)));
+  if (!range_start || !range_end) amax = nh_max(amax, nh_max(1.0, fabs(c11)));
   acc.r2 += res[0] * res[0] + res[1] * res[1] + res[2] * res[2] + res[3] * res[3];
   acc.b2 += r[0] * r[0] + r[1] * r[1] + r[2] * r[2] + b3 * b3;
   acc.x2 += P0 * P0 + Q0 * Q0 + P1 * P1 + Q1 * Q1;
-  acc.amax = fmax(acc.amax, amax);
+  acc.amax = nh_max(acc.amax, amax);
 }
 
 // A warp's residual shares into the member's running sums (all 32 lanes
@@ -374,7 +374,7 @@ NH_DEV void resid_flush_warp(nh_status* st, ResidAcc a) {
     a.r2 += __shfl_xor_sync(0xffffffffu, a.r2, o);
     a.b2 += __shfl_xor_sync(0xffffffffu, a.b2, o);
     a.x2 += __shfl_xor_sync(0xffffffffu, a.x2, o);
-    a.amax = fmax(a.amax, __shfl_xor_sync(0xffffffffu, a.amax, o));
+    a.amax = nh_max(a.amax, __shfl_xor_sync(0xffffffffu, a.amax, o));
   }
   if ((threadIdx.x & 31) == 0 && (a.amax > 0.0 || a.x2 > 0.0 || a.b2 > 0.0 || a.r2 != 0.0)) {
     atomicAdd(&st->resid_acc[0], a.r2);

@@ -57,6 +57,7 @@ void* nh_stream_kp_ptr();    // stream_kp.cu
 size_t nh_stream_kp_smem();  // its dynamic shared memory
 int nh_stream_kp_threads();  // its block size
 void* nh_stream_kp_fused_ptr();  // K_P with the K_S condensation fused in (global mode), or NULL
+void* nh_stream_kfin_ptr();      // K_fin: the last pending hw update over the flagged-tile list
 int nh_stream_kp_records_hw_any();   // 1: K_P records any(hw != 0) for the w / w_x fallback
 int nh_launch_gather_p(const double* pend, const uint8_t* flags, double* p, size_t n,
                        cudaStream_t s);

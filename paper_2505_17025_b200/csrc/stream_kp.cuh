@@ -462,7 +462,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
 // NH_HP_TRACES(ks), made visible by the caller's barrier.
 // hw += dt/rho (6/quad p + d_x/quad (h p)_x + phi) on flagged elements
 // (corrector.py:441-482); (h p)_x lifts use the neighbours' (h p) traces.
-template <bool FUSE, class SM>
+template <bool FUSE, bool FIN, class SM>
 __device__ __forceinline__ void kp_correct_and_step(const StreamArgs& a, const TileIdx& ti,
                                                     const nh_member& msh, const MemberConst& mc,
                                                     SM& ks, double* sq, Q6 q, bool f, double p0,
@@ -503,6 +503,13 @@ __device__ __forceinline__ void kp_correct_and_step(const StreamArgs& a, const T
     q.w0 += mc.lk.cdt * bp0;
     q.w1 += mc.lk.cdt * bp1;
   }
+  if (FIN) {   // K_fin: only flagged elements change (the tile is on the last step's list)
+    if (f && ti.own) {
+      double2 vw{q.w0, q.w1};
+      *reinterpret_cast<double2*>(const_cast<double*>(a.hw_in) + ti.o) = vw;
+    }
+    return;
+  }
   if (a.finalize) {
     if (ti.own) {
       double2 vw{q.w0, q.w1};
@@ -529,8 +536,9 @@ __device__ __forceinline__ void kp_correct_and_step(const StreamArgs& a, const T
   }
 }
 
-// One K_P tile (b, tile): the body of nh_stream_kp / nh_stream_kp_fused.
-template <bool FUSE>
+// One K_P tile (b, tile): the body of nh_stream_kp / nh_stream_kp_fused, and
+// (FIN) of nh_stream_kfin, which applies the last pending update only.
+template <bool FUSE, bool FIN = false>
 __device__ __forceinline__ void kp_tile(const StreamArgs& a, const TileIdx& ti, nh_member& msh,
                                         MemberConst& mc, KpSmem& ks) {
   const int N = a.N, i = ti.i, b = ti.b, e = ti.e;
@@ -557,5 +565,5 @@ __device__ __forceinline__ void kp_tile(const StreamArgs& a, const TileIdx& ti, 
     NH_HP_TRACES(ks)[1 * TPB + i] = q.h1 * p1;
   }
   __syncthreads();
-  kp_correct_and_step<FUSE>(a, ti, msh, mc, ks, ks.sq, q, f, p0, p1, phi0, phi1, dx0, dx1);
+  kp_correct_and_step<FUSE, FIN>(a, ti, msh, mc, ks, ks.sq, q, f, p0, p1, phi0, phi1, dx0, dx1);
 }
