@@ -31,6 +31,11 @@ from .scenarios import ScenarioSpec
 
 _MODES = {"hydrostatic": _lib.MODE_HYDROSTATIC, "global": _lib.MODE_GLOBAL,
           "adaptive": _lib.MODE_ADAPTIVE}
+# Longest member of the streaming path: K_X chains a member's tiles with one
+# warp, 8 tiles of 120 elements per lane (NH_STREAM_MAXCPL).  Longer members
+# (the reference has no limit) run the m-node kernels, whose chain is one
+# thread per member: correct at any length, at coverage speed.
+STREAM_MAX_ELEMENTS = 32 * 8 * 120
 
 
 @dataclass
@@ -97,9 +102,9 @@ class Ensemble:
         and config 4 (0.83 vs 4.4 ms/step), tools/scenario_paths.py,
         tools/path_compare.py.  Every mode and criterion runs on it (the w /
         w_x first-step fallback of adaptivity.py:153 is K_F); the resident
-        kernel stays available as path="resident".  Orders p > 1 run the
-        m-node kernels ("generic")."""
-        if self.M != 2:
+        kernel stays available as path="resident".  Orders p > 1, and members
+        longer than STREAM_MAX_ELEMENTS, run the m-node kernels ("generic")."""
+        if self.M != 2 or self.N > STREAM_MAX_ELEMENTS:
             return "generic"
         return "stream"
 
@@ -139,6 +144,10 @@ class Ensemble:
         sch = D.scheme(_MODES[mode], c.kind, c.k_nh, c.enlarge, flux, g, rho)
         if path == "auto":
             path = self.choose_path(mode, criterion)
+        if path == "stream" and self.N > STREAM_MAX_ELEMENTS:
+            path = "generic"   # longer members than K_X chains: the m-node kernels (no cap)
+        if path == "generic" and self.pm is None and self.M == 2:
+            self.pm = D.upload_members(D.pm_from_members(self.records))
         if mode != "hydrostatic" and (flux.c12 != -0.5 or flux.c22 != 0.0):
             # an LDG flux outside the alternating family: the m-node kernels'
             # band solve per range (P1 members: operators from their records)

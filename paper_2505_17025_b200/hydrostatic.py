@@ -97,6 +97,9 @@ def max_wavespeed(state: FlowState, g: float = GRAVITY) -> float:
     return float(T.max(T.abs(hu / h) + T.sqrt(g * h)).item())
 
 
+RESIDENT_MAX_ELEMENTS = 16 * (3 * 384 - 8)
+
+
 def _advance_one(state: FlowState, dt: float, bathy, bcs, mode: int, g: float, rho: float,
                  kind="eta_over_d", k_nh=1e-3, enlarge=False, flux=None, want_flags=False,
                  want_p=False, given=None):
@@ -107,7 +110,9 @@ def _advance_one(state: FlowState, dt: float, bathy, bcs, mode: int, g: float, r
     # run the m-node kernels (csrc/pm_kernels.cu)
     general = (mode != _lib.MODE_HYDROSTATIC and flux is not None
                and (flux.c12 != -0.5 or flux.c22 != 0.0))
-    pm = grid.poly_order != 1 or general
+    # ... and so do grids beyond the resident cluster kernel's capacity
+    # (16 CTAs x (3 x 384 - 8) elements; the reference has no size limit)
+    pm = grid.poly_order != 1 or general or grid.n_elements > RESIDENT_MAX_ELEMENTS
     m = D.upload_members(D.member_record(grid, bathy, bcs, dt, any_order=grid.poly_order != 1))
     h, hu, hw = _upload_state(state)
     t = D.dev(np.array([state.time]))

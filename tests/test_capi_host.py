@@ -32,7 +32,7 @@ def test_library_loads_and_exports_every_symbol():
     lib = _lib.load()
     for name in header_functions():
         assert getattr(lib, name) is not None
-    assert lib.nh_abi_version() == _lib.ABI_VERSION == 4
+    assert lib.nh_abi_version() == _lib.ABI_VERSION == 5
 
 
 def test_plan_host_logic():

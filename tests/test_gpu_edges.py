@@ -110,3 +110,34 @@ def test_stream_positivity_error_names_member_element_step():
     with pytest.raises(P.PositivityError) as ei:
         ens.check()
     assert ei.value.element == 187
+
+
+def test_members_longer_than_the_kernel_caps():
+    """The reference has no size limit.  A member longer than the streaming
+    path chains (32 x 8 tiles of 120 elements) and than the resident cluster
+    kernel holds runs the m-node kernels instead (driver.STREAM_MAX_ELEMENTS,
+    hydrostatic.RESIDENT_MAX_ELEMENTS): same results as the oracle, through
+    the ensemble loop and through the single-step API."""
+    from paper_2505_17025_b200.driver import STREAM_MAX_ELEMENTS
+    n = STREAM_MAX_ELEMENTS + 1000
+    grid = P.GridSpec(0.0, 400.0, n)
+    bcs = P.BoundaryPair(P.WALL, P.ABSORBING)
+    dt = 0.05 * grid.dx
+    h, hu, hw = bump_state(grid, 0.2, 150.0, 6.0)
+    crit = P.Criterion("eta_over_d", 1e-3, True)
+    steps = 4
+    ens = P.Ensemble.from_host(D.member_record(grid, P.FlatBottom(1.0), bcs, dt), h[None],
+                               hu[None], hw[None])
+    assert ens.choose_path("adaptive", crit) == "generic"
+    ens.advance(steps, "adaptive", crit)
+    stt = ens.check()
+    o = O.run(oracle_member(grid, P.FlatBottom(1.0), bcs, dt), h, hu, hw, steps, enlarge=True)
+    assert rel(ens.h[0].cpu().numpy() - 1.0, o.h - 1.0) <= 1e-9
+    assert rel(ens.hu[0].cpu().numpy(), o.hu) <= 1e-9
+    assert stt["flagged"][0] == round(o.fraction_mean * steps * n) > 0
+    st = P.FlowState(P.NodalField(grid, h), P.NodalField(grid, hu), P.NodalField(grid, hw), 0.0)
+    r = P.adaptive_step(st, dt, P.FlatBottom(1.0), bcs, mode="adaptive", crit=crit, cfl_warn=False)
+    o1 = O.step(oracle_member(grid, P.FlatBottom(1.0), bcs, dt), h, hu, hw, 0.0, "adaptive",
+                "eta_over_d", 1e-3, True)
+    assert np.array_equal(r.mask.flags, o1.flags)
+    assert rel(r.state.hu.values, o1.hu) <= 1e-12
