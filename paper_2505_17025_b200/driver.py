@@ -236,8 +236,18 @@ def advance_host(records: np.ndarray, h, hu, hw, time, n_steps: int, mode: str =
     s_in, s_cmp, s_out = T.cuda.Stream(), T.cuda.current_stream(), T.cuda.Stream()
     s_in.wait_stream(s_cmp)
     freed = [None] * NBUF      # event: the buffer's previous copy-out finished
-    for i, c0 in enumerate(range(0, B, block)):
-        c1 = min(B, c0 + block)
+    # block schedule: short blocks at both ends (block/4, block/2, block, ...,
+    # block/2, block/4), so the first compute starts after a quarter block's
+    # copy-in and only a quarter block's copy-out trails the last compute
+    ramp = [r for r in (block // 4, block // 2) if r >= 64]
+    head, tail = (ramp, ramp[::-1]) if B >= 2 * sum(ramp) + block else ([], [])
+    sizes = list(head)
+    left = B - sum(head) - sum(tail)
+    sizes += [block] * (left // block) + ([left % block] if left % block else [])
+    sizes += tail
+    starts = np.concatenate([[0], np.cumsum(sizes)]).astype(int)
+    for i, (c0, c1) in enumerate(zip(starts[:-1], starts[1:])):
+        c0, c1 = int(c0), int(c1)
         n, k = c1 - c0, i % NBUF
         buf = bufs[k]
         with T.cuda.stream(s_in):

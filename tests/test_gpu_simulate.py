@@ -176,6 +176,31 @@ def test_stream_member_chunks_bitwise_equal():
             assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("block", [None, 64, 300, 1000])
+def test_advance_host_bitwise_equal_to_device_ensemble(block):
+    """driver.advance_host (the end-to-end call of bench.py's e2e leg: pinned
+    host state streamed through the GPU in member blocks on three streams and
+    three device buffers, short blocks at both ends) leaves the host arrays
+    bit-identical to Ensemble.advance on the device-resident ensemble."""
+    import torch
+    from paper_2505_17025_b200.driver import advance_host
+    cfg = configs.Config4(n_members=700, n_elements=130, n_steps=21)
+    recs = cfg.records()
+    states = [cfg.host_state(i, oracle_depth) for i in range(cfg.n_members)]
+    H, Q, W = (np.stack([s[k] for s in states]) for k in range(3))
+    crit = P.Criterion("eta_over_d")
+    ens = P.Ensemble.from_host(recs, H, Q, W)
+    ens.advance(cfg.n_steps, "adaptive", crit)
+    st = ens.check()
+    host = [torch.from_numpy(x.copy()).pin_memory() for x in (H, Q, W)]
+    t = torch.zeros(cfg.n_members, dtype=torch.float64).pin_memory()
+    st2 = advance_host(recs, *host, t, cfg.n_steps, "adaptive", crit, block=block)
+    for a, b in zip(host + [t], (ens.h, ens.hu, ens.hw, ens.time)):
+        assert torch.equal(a, b.cpu())
+    assert np.array_equal(st2["flagged"], st["flagged"])
+    assert (st2["error_key"] == st["error_key"]).all()
+
+
 @pytest.mark.parametrize("n_steps", [5, 6, 61])
 @pytest.mark.parametrize("mode", ["adaptive", "global", "hydrostatic"])
 def test_stream_graph_bitwise_equal_to_launches(n_steps, mode):
