@@ -39,7 +39,6 @@ struct BottomTime {
 // det_log1p): IEEE +,-,* only -- Cody-Waite reduction and Horner polynomials,
 // explicit round-to-nearest intrinsics (never contracted), same constants and
 // order as the numpy definition, so host and device round identically.
-#if NH_OPT_EXPC
 // the Horner coefficients as constant-bank operands of the DADDs (as
 // immediates every coefficient costs two uniform-register moves)
 static __constant__ double NH_EXP_COEF[14] = {
@@ -47,20 +46,12 @@ static __constant__ double NH_EXP_COEF[14] = {
     2.755731922398589e-07,  2.7557319223985893e-06, 2.48015873015873e-05,
     0.0001984126984126984,  0.001388888888888889, 0.008333333333333333,
     0.041666666666666664,   0.16666666666666666, 0.5, 1.0, 1.0};
-#endif
 
 __device__ __forceinline__ double nh_det_exp(double x) {
   const double k = rint(__dmul_rn(x, 1.4426950408889634));
   const double r = __dsub_rn(__dsub_rn(x, __dmul_rn(k, 0.6931471803691238)),
                              __dmul_rn(k, 1.9082149292705877e-10));
-#if NH_OPT_EXPC
   const double* c = NH_EXP_COEF;
-#else
-  const double c[14] = {1.6059043836821613e-10, 2.08767569878681e-09, 2.505210838544172e-08,
-                        2.755731922398589e-07,  2.7557319223985893e-06, 2.48015873015873e-05,
-                        0.0001984126984126984,  0.001388888888888889, 0.008333333333333333,
-                        0.041666666666666664,   0.16666666666666666, 0.5, 1.0, 1.0};
-#endif
   double p = c[0];
 #pragma unroll
   for (int n = 1; n < 14; ++n) p = __dadd_rn(__dmul_rn(p, r), c[n]);
@@ -83,14 +74,7 @@ __device__ __forceinline__ void nh_det_exp2(double xa, double xb, double& ya, do
                               __dmul_rn(ka, 1.9082149292705877e-10));
   const double rb = __dsub_rn(__dsub_rn(xb, __dmul_rn(kb, 0.6931471803691238)),
                               __dmul_rn(kb, 1.9082149292705877e-10));
-#if NH_OPT_EXPC
   const double* c = NH_EXP_COEF;
-#else
-  const double c[14] = {1.6059043836821613e-10, 2.08767569878681e-09, 2.505210838544172e-08,
-                        2.755731922398589e-07,  2.7557319223985893e-06, 2.48015873015873e-05,
-                        0.0001984126984126984,  0.001388888888888889, 0.008333333333333333,
-                        0.041666666666666664,   0.16666666666666666, 0.5, 1.0, 1.0};
-#endif
   double pa = c[0], pb = c[0];
 #pragma unroll
   for (int n = 1; n < 14; ++n) {
@@ -323,7 +307,6 @@ template <int KIND>
 __device__ __forceinline__ void bottom_eval_sp2(const nh_member& m, const BottomTime& bt,
                                                 double x0, double x1, const BottomSpace& s0,
                                                 const BottomSpace& s1, Bottom6& b0, Bottom6& b1) {
-#if NH_OPT_EXP2
   if (KIND == NH_BOTTOM_SLOPE_SLIDE) {
     const double* p = m.bottom;
     const double ramp0 = RADD(p[0], RMUL(x0, p[1])), ramp1 = RADD(p[0], RMUL(x1, p[1]));
@@ -349,7 +332,6 @@ __device__ __forceinline__ void bottom_eval_sp2(const nh_member& m, const Bottom
     }
     return;
   }
-#endif
   b0 = bottom_eval_sp<KIND>(m, bt, x0, s0);
   b1 = bottom_eval_sp<KIND>(m, bt, x1, s1);
 }

@@ -121,11 +121,7 @@ NH_DEV Face face_flux(const Side& L, const Side& R, double g, double& speed) {
     // hw stays identically 0 where no correction has ever acted)
     if (WARP) {
       wL = L.hw; wR = R.hw;
-#if NH_OPT_HWZERO
       const bool nL = hLs != L.h && L.hw != 0.0, nR = hRs != R.h && R.hw != 0.0;
-#else
-      const bool nL = hLs != L.h, nR = hRs != R.h;
-#endif
       if (__any_sync(0xffffffffu, nL || nR)) {
         bool bad = false;
         double rL = nh_div_pos_fp(hLs, L.h, bad), rR = nh_div_pos_fp(hRs, R.h, bad);

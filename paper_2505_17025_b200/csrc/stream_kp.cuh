@@ -322,7 +322,6 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
     // the default criterion, evaluated by the whole warp (one vote for both
     // divisions); halo slots past the domain ends compute and discard
     const double e0 = RSUB(qp.h0, d0), e1 = RSUB(qp.h1, d1);
-#if NH_OPT_CRIT
     // |e / d| > k decided without the division wherever that is certain:
     // with p = k d, |e| >= p (1 + 2^-50) puts e / d more than an ulp above k
     // and |e| <= p (1 - 2^-50) more than an ulp below it, so the rounded
@@ -337,12 +336,6 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
     bool hit = sure;
     NH_WARP_FIX(amb, (hit = sure || nh_max(fabs(RDIVP(e0, d0)), fabs(RDIVP(e1, d1))) > k));
     raw = (valid && hit) ? 1 : 0;
-#else
-    bool badc = false;
-    double v0 = fabs(nh_div_pos_fp(e0, d0, badc)), v1 = fabs(nh_div_pos_fp(e1, d1, badc));
-    NH_WARP_FIX(badc, (v0 = fabs(RDIVP(e0, d0)), v1 = fabs(RDIVP(e1, d1))));
-    raw = (valid && nh_max(v0, v1) > sch.k_nh) ? 1 : 0;
-#endif
   } else
 #endif
   if (valid && sch.mode != NH_MODE_HYDROSTATIC) {

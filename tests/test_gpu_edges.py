@@ -141,3 +141,34 @@ def test_members_longer_than_the_kernel_caps():
                 "eta_over_d", 1e-3, True)
     assert np.array_equal(r.mask.flags, o1.flags)
     assert rel(r.state.hu.values, o1.hu) <= 1e-12
+
+
+def test_criterion_at_the_threshold():
+    """K_P decides |eta / d| > k_nh without the division wherever the product
+    comparison is certain and divides only inside a 2^-49 band around the
+    threshold.  Uniform members at rest keep h exactly (zero tendencies), so
+    eta / d is controlled to the bit: exactly k_nh (inside the band; not
+    flagged, the comparison is strict) and one ulp of h to either side."""
+    k = 2.0 ** -10
+    n = 130
+    grid = P.GridSpec(0.0, 10.0, n)
+    bcs = P.BoundaryPair(P.WALL, P.WALL)
+    dt = 0.01 * grid.dx
+    hs = [1.0 + k, np.nextafter(1.0 + k, 2.0), np.nextafter(1.0 + k, 0.0), 1.0 - k,
+          np.nextafter(1.0 - k, 0.0), np.nextafter(1.0 - k, 2.0)]
+    recs = np.concatenate([D.member_record(grid, P.FlatBottom(1.0), bcs, dt) for _ in hs])
+    H = np.stack([np.full((n, 2), v) for v in hs])
+    Z = np.zeros_like(H)
+    crit = P.Criterion("eta_over_d", k, False)
+    for path in ("stream", "resident"):
+        ens = P.Ensemble.from_host(recs, H, Z, Z)
+        ens.advance(1, "adaptive", crit, path=path)
+        st = ens.check()
+        want = []
+        for v in hs:
+            o = O.step(oracle_member(grid, P.FlatBottom(1.0), bcs, dt), np.full((n, 2), v),
+                       Z[0], Z[0], 0.0, "adaptive", "eta_over_d", k, False)
+            assert np.array_equal(o.h, np.full((n, 2), v))   # at rest: h exact
+            want.append(int(o.flags.sum()))
+        assert want == [0, n, 0, 0, n, 0], want
+        assert list(st["flagged"]) == want, (path, list(st["flagged"]))
