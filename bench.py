@@ -453,6 +453,8 @@ def run_b200(args):
                          "fp64": {"kp_fp64_pipe_active_pct":
                                       (traffic_src or {}).get("fp64_pipe_active_pct"),
                                   "kp_issue_active_pct": (traffic_src or {}).get("issue_active_pct"),
+                                  "kp_fp64_arith_frac_of_peak":
+                                      (traffic_src or {}).get("fp64_arith_frac_of_peak"),
                                   "measured_dfma_peak_tflops": fp64.get("tflops"),
                                   "source": "ncu --set full of K_P (profiles/) and "
                                             "profiles/fp64_peak.json"},

@@ -38,6 +38,14 @@ def main(rep, pattern, out, workload="config4", cells=None):
                                          "nan").replace(",", "")),
             "issue_active_pct": float(d.get("smsp__issue_active.avg.pct_of_peak_sustained_active",
                                             "nan").replace(",", "")),
+            # fp64 arithmetic (thread-level DADD + DMUL + DFMA per cycle, whole GPU)
+            # against the pipe's peak (64 per clock per SM)
+            "fp64_ops_per_cycle": sum(float(d.get(
+                f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed", "0")
+                .replace(",", "")) for op in ("dadd", "dmul", "dfma")),
+            "fp64_peak_per_cycle": float(d.get(
+                "sm__sass_thread_inst_executed_op_dfma_pred_on.sum.peak_sustained", "nan")
+                .replace(",", "")),
         })
     r0 = recs[0]
     res = {"source": rep.split("/")[-1], "workload": workload, "kernel": r0["kernel"], "grid": r0["grid"],
@@ -45,7 +53,8 @@ def main(rep, pattern, out, workload="config4", cells=None):
            "dram_bytes_per_launch": r0["dram_read_bytes"] + r0["dram_write_bytes"],
            "dram_read_bytes": r0["dram_read_bytes"], "dram_write_bytes": r0["dram_write_bytes"],
            "ncu_duration_ms": r0["duration_ms"], "launches_captured": len(recs),
-           "fp64_pipe_active_pct": r0["fp64_pipe_pct"], "issue_active_pct": r0["issue_active_pct"]}
+           "fp64_pipe_active_pct": r0["fp64_pipe_pct"], "issue_active_pct": r0["issue_active_pct"],
+           "fp64_arith_frac_of_peak": r0["fp64_ops_per_cycle"] / r0["fp64_peak_per_cycle"]}
     if cells:
         res["cells_per_launch"] = int(cells)
         res["dram_bytes_per_cell"] = res["dram_bytes_per_launch"] / int(cells)
