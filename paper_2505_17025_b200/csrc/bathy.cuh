@@ -59,7 +59,7 @@ __device__ __forceinline__ double nh_det_exp(double x) {
   // normal number -- the correctly rounded p 2^k, i.e. scalbn(p, k) bit for
   // bit (the library call is a dozen integer instructions)
   const int ki = (int)k;
-  if (ki >= -1022 && ki <= 1023)
+  if (NH_LIKELY(ki >= -1022 && ki <= 1023))
     return __dmul_rn(p, __longlong_as_double((long long)(ki + 1023) << 52));
   return scalbn(p, ki);
 }
@@ -82,7 +82,7 @@ __device__ __forceinline__ void nh_det_exp2(double xa, double xb, double& ya, do
     pb = __dadd_rn(__dmul_rn(pb, rb), c[n]);
   }
   const int ia = (int)ka, ib = (int)kb;
-  if (ia >= -1022 && ia <= 1023 && ib >= -1022 && ib <= 1023) {
+  if (NH_LIKELY(ia >= -1022 && ia <= 1023 && ib >= -1022 && ib <= 1023)) {
     ya = __dmul_rn(pa, __longlong_as_double((long long)(ia + 1023) << 52));
     yb = __dmul_rn(pb, __longlong_as_double((long long)(ib + 1023) << 52));
   } else {

@@ -45,7 +45,7 @@ __device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q
   sh[4 * TPB + i] = n1.u;
   __syncthreads();
   Side L;
-  if (e == 0) {
+  if (NH_UNLIKELY(e == 0)) {
     L = ghost_side(n0, m.bc_left);
   } else {   // the left neighbour's node-1 side, u included (no second division)
     int k = i > 0 ? i - 1 : 0;
@@ -63,7 +63,7 @@ __device__ __forceinline__ void stage_tend(const nh_member& m, double g, const Q
   sf[0 * TPB + i] = fl.F1; sf[1 * TPB + i] = fl.F2L; sf[2 * TPB + i] = fl.F3;
   __syncthreads();
   Face fr;
-  if (e == N - 1) {
+  if (NH_UNLIKELY(e == N - 1)) {
     fr = face_flux<KIND == NH_BOTTOM_FLAT>(n1, ghost_side(n1, m.bc_right), g, sp);
     speed = nh_max(speed, sp);
   } else {
@@ -375,7 +375,7 @@ __device__ __forceinline__ void kp_body(const StreamArgs& a, const nh_member& m,
   }
   rf[i] = raw;
   __syncthreads();
-  if (bad)   // the reference raises at the first failing check: lowest code wins
+  if (NH_UNLIKELY(bad))   // the reference raises at the first failing check: lowest code wins
     nh_report(st, step,
               (bad & 1u) ? NH_ERR_POSITIVITY_ENTRY
                          : ((bad & 2u) ? NH_ERR_POSITIVITY_STAGE1 : NH_ERR_POSITIVITY_STAGE2),
