@@ -289,6 +289,18 @@ int nh_criterion(const nh_member* members, int n_members, int n_elements,
                  const double* h, const double* hu, const double* hw, const double* time,
                  int kind, double* values, void* stream);
 
+/* evaluate_criterion's mask (adaptivity.py:99-113) from nodal indicator
+ * values [B][N][nodes] (nh_criterion / nh_pm_criterion): flags[b][e] = max
+ * over the element's nodes > k_nh, with the optional +-1 enlargement clipped
+ * to the member. */
+int nh_mask(const double* values, int n_members, int n_elements, int nodes, double k_nh,
+            int enlarge, uint8_t* flags, void* stream);
+
+/* max_wavespeed (hydrostatic.py:187-189): out[b] = max over the member's
+ * nodes of |hu / h| + sqrt(g h), IEEE division and square root. */
+int nh_max_wavespeed(const double* h, const double* hu, int n_members,
+                     long long nodes_per_member, double g, double* out, void* stream);
+
 /* Elliptic coefficients on all elements, corrector.phi_term +
  * assemble_coefficients (corrector.py:100-170).  coef [7][B][N][2] =
  * s11, s12, s22, f1, f2, phi, d_x (s21 = -s11). */

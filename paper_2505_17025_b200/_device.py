@@ -265,6 +265,21 @@ def pm_advance(members, pm, h, hu, hw, time, n_steps, sch, status, flag_bits=Non
     _lib.check(rc, "nh_pm_advance")
 
 
+class nvtx_range:
+    """NVTX range around a block of launches (shows in Nsight timelines;
+    a no-op cost when no profiler is attached)."""
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        torch().cuda.nvtx.range_push(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        torch().cuda.nvtx.range_pop()
+
+
 def stream_workspace(B: int, N: int):
     lib = require_cuda()
     n = int(lib.nh_stream_workspace_bytes(B, N))

@@ -62,7 +62,7 @@ class Outputs(ctypes.Structure):
 ABI_VERSION = 5   # include/nhswe_b200.h NH_ABI_VERSION
 
 EXPORTS = ("nh_abi_version", "nh_advance", "nh_stream_advance", "nh_stream_workspace_bytes",
-           "nh_rhs", "nh_criterion", "nh_coefficients",
+           "nh_rhs", "nh_criterion", "nh_mask", "nh_max_wavespeed", "nh_coefficients",
            "nh_ldg_solve", "nh_correct_momentum", "nh_bottom_sample", "nh_plan",
            "nh_last_cuda_error", "nh_stream_graphs", "nh_stream_timing", "nh_stream_kernel_times",
            "nh_launch_count",
@@ -87,6 +87,8 @@ _SIGS = {
     "nh_rhs": ([_P, _I, _I, _P, _P, _P, _P, _D, _P, _P, _P, _P, _P], _I),
     "nh_criterion": ([_P, _I, _I, _P, _P, _P, _P, _I, _P, _P], _I),
     "nh_coefficients": ([_P, _I, _I, _P, _P, _P, _P, _D, _D, _P, _P], _I),
+    "nh_mask": ([_P, _I, _I, _I, _D, _I, _P, _P], _I),
+    "nh_max_wavespeed": ([_P, _P, _I, ctypes.c_longlong, _D, _P, _P], _I),
     "nh_ldg_solve": ([_P, _I, _I, _P, _P, _P, _P, _D, _D, _D, _D, _D, _P, _P, _P, _P], _I),
     "nh_correct_momentum": ([_P, _I, _I, _P, _P, _P, _P, _D, _P, _P, _P], _I),
     "nh_bottom_sample": ([_P, _I, _P, _I, _P, _P, _P], _I),

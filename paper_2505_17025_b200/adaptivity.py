@@ -108,14 +108,13 @@ def evaluate_criterion(predictor: FlowState, bathy: BathymetryModel,
                        crit: Criterion) -> NonHydroMask:
     """Flag = max nodal indicator > k_nh, optional enlargement (adaptivity.py:107-113)."""
     T = D.torch()
-    v = _criterion_device(predictor, bathy, crit.kind)
-    f = T.amax(v, dim=1) > crit.k_nh
-    if crit.enlarge:
-        g = f.clone()
-        g[:-1] |= f[1:]
-        g[1:] |= f[:-1]
-        f = g
-    return NonHydroMask.from_flags(f.cpu().numpy())
+    lib = D.require_cuda()
+    v = _criterion_device(predictor, bathy, crit.kind).contiguous()
+    n, m = int(v.shape[0]), int(v.shape[1])
+    flags = T.empty(n, dtype=T.uint8, device="cuda")
+    _lib.check(lib.nh_mask(D.ptr(v), 1, n, m, float(crit.k_nh), 1 if crit.enlarge else 0,
+                           D.ptr(flags), D.stream_ptr()), "nh_mask")
+    return NonHydroMask.from_flags(flags.cpu().numpy().astype(bool))
 
 
 def full_mask(n_elements: int) -> NonHydroMask:

@@ -4,6 +4,7 @@
 // ldg_solve / solve_on_ranges.  The fused time step (step_kernel.cu) does not
 // use these; they exist so every public function of the reference hot path
 // has a device implementation of its own (no CPU fallback).
+#include <algorithm>
 #include <cooperative_groups.h>
 #include "bathy.cuh"
 #include "physics.cuh"
@@ -346,7 +347,61 @@ __global__ void nh_selftest_kernel(long long n, unsigned long long seed, unsigne
   if (np) atomicAdd(bad + 2, np);
 }
 
+// evaluate_criterion's mask (adaptivity.py:99-113): flag = max nodal indicator
+// of the element > k_nh, optionally dilated by one element to each side
+// (clipped to the member).  One thread per element; values [B][N][m].
+__global__ void nh_mask_kernel(const double* __restrict__ v, int B, int N, int m, double k_nh,
+                               int enlarge, uint8_t* __restrict__ flags) {
+  const size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (idx >= (size_t)B * N) return;
+  const int e = (int)(idx % N);
+  auto raw = [&](size_t i) -> bool {
+    double mx = v[i * m];
+    for (int j = 1; j < m; ++j) mx = fmax(mx, v[i * m + j]);   // np.max: NaN-free here
+    return mx > k_nh;
+  };
+  bool f = raw(idx);
+  if (enlarge) {
+    if (e > 0) f = f || raw(idx - 1);
+    if (e < N - 1) f = f || raw(idx + 1);
+  }
+  flags[idx] = f ? 1 : 0;
+}
+
+// max_wavespeed (hydrostatic.py:187-189): max over a member's nodes of
+// |hu / h| + sqrt(g h), every operation the IEEE-rounded one numpy does.
+// The values are non-negative, so the maximum is taken on the bit patterns.
+__global__ void nh_wavespeed_kernel(const double* __restrict__ h, const double* __restrict__ hu,
+                                    int B, size_t nodes, double g,
+                                    unsigned long long* __restrict__ out) {
+  const int b = blockIdx.y;
+  unsigned long long mx = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nodes;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const double hh = h[(size_t)b * nodes + i], q = hu[(size_t)b * nodes + i];
+    const double a = __dadd_rn(fabs(__ddiv_rn(q, hh)), __dsqrt_rn(__dmul_rn(g, hh)));
+    if (a == a) mx = max(mx, (unsigned long long)__double_as_longlong(a));
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(out + b, mx);
+}
+
 extern "C" {
+
+int nh_launch_mask(const double* values, int B, int N, int m, double k_nh, int enlarge,
+                   uint8_t* flags, cudaStream_t s) {
+  const size_t n = (size_t)B * N;
+  nh_mask_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(values, B, N, m, k_nh, enlarge, flags);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int nh_launch_wavespeed(const double* h, const double* hu, int B, size_t nodes, double g,
+                        double* out, cudaStream_t s) {
+  if (cudaMemsetAsync(out, 0, 8 * (size_t)B, s) != cudaSuccess) return 1;
+  const unsigned gx = (unsigned)std::min<size_t>((nodes + 255) / 256, 1024);
+  nh_wavespeed_kernel<<<dim3(gx, B), 256, 0, s>>>(h, hu, B, nodes, g, (unsigned long long*)out);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
 
 int nh_launch_selftest(long long n, unsigned long long seed, unsigned long long* bad,
                        cudaStream_t s) {

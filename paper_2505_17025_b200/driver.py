@@ -140,6 +140,10 @@ class Ensemble:
             raise ValueError(f"unknown mode {mode!r}")
         if mode == "adaptive" and criterion is None:
             raise ValueError("adaptive mode requires a criterion")
+        with D.nvtx_range(f"nhswe.advance[{mode}] B={self.B} N={self.N} steps={n_steps}"):
+            self._advance(n_steps, mode, criterion, flux, g, rho, flag_bits, p_out, path, gauges)
+
+    def _advance(self, n_steps, mode, criterion, flux, g, rho, flag_bits, p_out, path, gauges):
         c = criterion if criterion is not None else Criterion("eta_over_d")
         sch = D.scheme(_MODES[mode], c.kind, c.k_nh, c.enlarge, flux, g, rho)
         if path == "auto":
@@ -258,7 +262,7 @@ def advance_host(records: np.ndarray, h, hu, hw, time, n_steps: int, mode: str =
             loaded = T.cuda.Event()
             loaded.record(s_in)
         s_cmp.wait_event(loaded)
-        with T.cuda.stream(s_cmp):
+        with T.cuda.stream(s_cmp), D.nvtx_range(f"nhswe.advance_host block {c0}:{c1}"):
             D.stream_advance(members[c0 * rec:c1 * rec], buf[0][:n], buf[1][:n], buf[2][:n],
                              buf[3][:n], n_steps, sch, status[c0 * stb:c1 * stb], ws)
             done = T.cuda.Event()

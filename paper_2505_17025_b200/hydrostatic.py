@@ -90,11 +90,14 @@ def rhs_operator(state: FlowState, bathy: BathymetryModel, bcs: BoundaryPair,
 
 def max_wavespeed(state: FlowState, g: float = GRAVITY) -> float:
     """max |u| + sqrt(g h) (hydrostatic.py:187-189), reduced on the device."""
-    D.require_cuda()
+    lib = D.require_cuda()
     T = D.torch()
     h = D.dev(state.h.values)
     hu = D.dev(state.hu.values)
-    return float(T.max(T.abs(hu / h) + T.sqrt(g * h)).item())
+    out = T.zeros(1, dtype=T.float64, device="cuda")
+    _lib.check(lib.nh_max_wavespeed(D.ptr(h), D.ptr(hu), 1, int(h.numel()), float(g), D.ptr(out),
+                                    D.stream_ptr()), "nh_max_wavespeed")
+    return float(out.item())
 
 
 RESIDENT_MAX_ELEMENTS = 16 * (3 * 384 - 8)

@@ -237,3 +237,36 @@ def test_inline_ieee_division_and_sqrt_match_cuda():
     assert lib.nh_selftest_arith(n, 20251020, bad.data_ptr(), D.stream_ptr()) == 0
     torch.cuda.synchronize()
     assert bad.tolist() == [0, 0, 0]
+
+
+@pytest.mark.parametrize("enlarge", [False, True])
+@pytest.mark.parametrize("kind", ["eta_over_d", "u_x", "w"])
+def test_evaluate_criterion_and_max_wavespeed(kind, enlarge):
+    """evaluate_criterion (adaptivity.py:107-113: nh_criterion + nh_mask on
+    the device) equals the oracle's thresholded, enlarged indicator and the
+    mask adaptive_step applies; max_wavespeed (hydrostatic.py:187-189,
+    nh_max_wavespeed) equals the numpy expression bit for bit."""
+    import paper_2505_17025_b200 as P
+    from tests.test_gpu_golden import pkg_case
+    from tests.helpers import oracle_member
+    for name in ("flat_walls", "plate", "slope_slide"):
+        g, b, bcs, dt, st = pkg_case(name)
+        for _ in range(3):   # a developed state (nonzero hw for the w criterion)
+            st = P.adaptive_step(st, dt, b, bcs, mode="global", cfl_warn=False).state
+        pred = P.heun_step(st, dt, b, bcs, cfl_warn=False)
+        k = 0.5 * float(np.abs(P.criterion_values(pred, b, kind)).max()) or 1e-3
+        crit = P.Criterion(kind, k, enlarge)
+        mask = P.evaluate_criterion(pred, b, crit)
+        mem = oracle_member(g, b, bcs, dt)
+        v = O.indicator(mem.grid, mem.bottom, kind, pred.h.values, pred.hu.values,
+                        pred.hw.values, pred.time)
+        want = v.max(axis=1) > k
+        if enlarge:
+            want = P.enlarge_flags(want)
+        assert 0 < want.sum() < want.size
+        assert np.array_equal(mask.flags, want), (name, kind)
+        assert mask.ranges == P.contiguous_ranges(want)
+        step = P.adaptive_step(st, dt, b, bcs, mode="adaptive", crit=crit, cfl_warn=False)
+        assert np.array_equal(step.mask.flags, mask.flags)
+        h, hu = pred.h.values, pred.hu.values
+        assert P.max_wavespeed(pred) == float(np.max(np.abs(hu / h) + np.sqrt(9.81 * h)))
