@@ -146,7 +146,10 @@ int nh_abi_version(void);
  * with NH_MODE_CORRECT_GIVEN it is corrector.apply_correction
  * (corrector.py:485-498).  `time` [B] holds each member's t and is advanced
  * by t += dt per step (hydrostatic.py:206-209).  `status` [B] is
- * zero-initialised by the caller except error_key = ~0. */
+ * zero-initialised by the caller except error_key = ~0.
+ * Limits (NH_E_UNSUPPORTED beyond them; nh_pm_advance with m = 2 has none):
+ * n_elements <= 16 CTAs x (3 x 384 - 8) = 18304 per member (one cluster owns a
+ * member); the alternating LDG flux family c12 = -1/2, c22 = 0 (any c11). */
 int nh_advance(const nh_member* members, int n_members, int n_elements,
                double* h, double* hu, double* hw, double* time, int n_steps,
                const nh_scheme* scheme, const nh_outputs* outputs,
@@ -158,8 +161,13 @@ int nh_advance(const nh_member* members, int n_members, int n_elements,
  * independent 120-element tiles of 128 threads (K_P predictor+criterion, K_S condensation,
  * K_X per-member tile chain, K_C reconstruction) with the vertical-momentum
  * update fused into the next step's load; state goes through HBM once per
- * step.  `workspace` is device memory of at least
- * nh_stream_workspace_bytes(B, N) bytes. */
+ * step; after the loop K_fin applies the last pending update on the flagged
+ * tiles.  `workspace` is device memory of at least
+ * nh_stream_workspace_bytes(B, N) bytes.
+ * Limits (NH_E_UNSUPPORTED beyond them; nh_pm_advance with m = 2 has none):
+ * n_elements <= 32 x 8 x 120 = 30720 per member (K_X chains a member's
+ * tiles with one warp); n_members x tiles < 2^31; the alternating LDG flux
+ * family. */
 int nh_stream_advance(const nh_member* members, int n_members, int n_elements,
                       double* h, double* hu, double* hw, double* time, int n_steps,
                       const nh_scheme* scheme, const nh_outputs* outputs,
@@ -179,7 +187,7 @@ int nh_stream_graphs(int enable);
  * roofline report).  nh_stream_timing(1) clears and arms the recorder; every
  * later nh_stream_advance brackets each launch with events on its stream.
  * nh_stream_kernel_times waits for the last event and returns, per kernel
- * [K_P, K_S, K_X, K_C, finalising K_P, prep], the summed milliseconds and launch
+ * [K_P, K_S, K_X, K_C, K_fin, prep], the summed milliseconds and launch
  * counts since arming, then clears (timing stays armed until
  * nh_stream_timing(0)). */
 #define NH_STREAM_NKERNELS 6

@@ -168,9 +168,12 @@ __device__ __forceinline__ TileIdx tile_idx(const StreamArgs& a, int b, int tile
   t.b = b; t.tile = tile;
   t.i = threadIdx.x; t.lane = t.i & 31; t.warp = t.i >> 5;
   t.e = t.tile * OWN - H + t.i;
-  t.valid = t.e >= 0 && t.e < a.N;
-  t.own = t.valid && t.i >= H && t.i < H + OWN;
-  t.o = ((size_t)t.b * a.N + (t.valid ? t.e : 0)) * 2;
+  // one unsigned compare per range test; o is only dereferenced for valid
+  // slots, so it is not clamped (CTA-uniform base + slot): cheaper to
+  // re-materialise, which the 64-register cap forces a dozen times
+  t.valid = (unsigned)t.e < (unsigned)a.N;
+  t.own = t.valid && (unsigned)(t.i - H) < (unsigned)OWN;
+  t.o = (size_t)((long long)t.b * a.N + (t.tile * OWN - H) + t.i) * 2;
   return t;
 }
 
