@@ -402,8 +402,15 @@ __global__ void __launch_bounds__(TPB, NH_KS_MIN_BLOCKS) nh_stream_kc(StreamArgs
   __shared__ KcSmem kc;
   const bool all = a.sch.mode == NH_MODE_GLOBAL;
   const int n = all ? a.B * a.tiles : *a.tile_count;
+  // the next tile's list entry is requested while the current tile runs: one
+  // dependent global load less at the head of every tile (K_C -2 %; the same
+  // in K_S measured +4 % on config 5, profiles/r2_ab_tile_prefetch.txt)
+  int bt = (!all && (int)blockIdx.x < n) ? a.tile_list[blockIdx.x] : 0;
   for (int w = blockIdx.x; w < n; w += gridDim.x) {
-    kc_tile(a, all ? w : a.tile_list[w], kc);
+    const int wn = w + gridDim.x;
+    const int nxt = (!all && wn < n) ? a.tile_list[wn] : 0;
+    kc_tile(a, all ? w : bt, kc);
+    bt = nxt;
     __syncthreads();   // shared memory is reused by the next tile
   }
 }
