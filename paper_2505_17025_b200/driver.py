@@ -200,6 +200,20 @@ class Ensemble:
         return st
 
 
+def block_schedule(n_members: int, block: int) -> list[int]:
+    """Member-block sizes of advance_host's pipeline: short blocks at both
+    ends (block/4, block/2, block, ..., block/2, block/4), so the first
+    compute starts after a quarter block's copy-in and only a quarter block's
+    copy-out trails the last compute.  Sums to n_members; no block exceeds
+    `block` (the workspace is sized for it)."""
+    block = max(1, min(n_members, block))
+    ramp = [r for r in (block // 4, block // 2) if r >= 64]
+    head, tail = (ramp, ramp[::-1]) if n_members >= 2 * sum(ramp) + block else ([], [])
+    left = n_members - sum(head) - sum(tail)
+    return (list(head) + [block] * (left // block) + ([left % block] if left % block else [])
+            + list(tail))
+
+
 def advance_host(records: np.ndarray, h, hu, hw, time, n_steps: int, mode: str = "adaptive",
                  criterion: Criterion | None = None, block: int | None = None,
                  flux: FluxCoefficients = FluxCoefficients(), g: float = 9.81,
@@ -240,16 +254,7 @@ def advance_host(records: np.ndarray, h, hu, hw, time, n_steps: int, mode: str =
     s_in, s_cmp, s_out = T.cuda.Stream(), T.cuda.current_stream(), T.cuda.Stream()
     s_in.wait_stream(s_cmp)
     freed = [None] * NBUF      # event: the buffer's previous copy-out finished
-    # block schedule: short blocks at both ends (block/4, block/2, block, ...,
-    # block/2, block/4), so the first compute starts after a quarter block's
-    # copy-in and only a quarter block's copy-out trails the last compute
-    ramp = [r for r in (block // 4, block // 2) if r >= 64]
-    head, tail = (ramp, ramp[::-1]) if B >= 2 * sum(ramp) + block else ([], [])
-    sizes = list(head)
-    left = B - sum(head) - sum(tail)
-    sizes += [block] * (left // block) + ([left % block] if left % block else [])
-    sizes += tail
-    starts = np.concatenate([[0], np.cumsum(sizes)]).astype(int)
+    starts = np.concatenate([[0], np.cumsum(block_schedule(B, block))]).astype(int)
     for i, (c0, c1) in enumerate(zip(starts[:-1], starts[1:])):
         c0, c1 = int(c0), int(c1)
         n, k = c1 - c0, i % NBUF

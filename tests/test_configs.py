@@ -53,3 +53,17 @@ def test_config5_table_admissible():
         assert np.allclose(rec["bottom"][i, :len(params)], params, rtol=1e-15)
         d = oracle_depth(m.bathymetry, m.grid.sample_nodes, 0.0)
         assert d.min() >= 0.04
+
+
+def test_advance_host_block_schedule():
+    """driver.block_schedule: the member blocks of the host-pipelined advance
+    cover the ensemble exactly, never exceed the workspace's block, and ramp
+    up and down at the ends when the ensemble is long enough."""
+    from paper_2505_17025_b200.driver import block_schedule
+    for n, blk in ((65536, 2048), (100, 2048), (5000, 2048), (4096, 2048), (3100, 1024),
+                   (1, 1), (700, 64), (700, 300), (129, 128)):
+        s = block_schedule(n, blk)
+        assert sum(s) == n and all(0 < v <= min(n, blk) for v in s), (n, blk, s)
+    s = block_schedule(65536, 2048)
+    assert s[:3] == [512, 1024, 2048] and s[-2:] == [1024, 512]
+    assert block_schedule(100, 2048) == [100]
