@@ -33,3 +33,16 @@ def test_reference_arm_json_line():
         assert cb["kind"] == "reference"
     e = d["e2e"]
     assert e["value"] == d["value"] and e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
+
+
+def test_cpu_leg_falls_back_to_the_oracle_port(monkeypatch):
+    """Without baseline/_ref the CPU legs run the oracle port (labelled
+    "port"); with it, the reference's own adaptive_step ("reference")."""
+    sys.path.insert(0, ROOT)
+    import bench
+    monkeypatch.setenv("NH_CPU_ARM", "port")
+    cells, secs, kind = bench._cpu_worker(("config4", 1, 1, 2, "adaptive"))
+    assert kind == "port" and cells == 2 * 4096 and secs > 0
+    monkeypatch.delenv("NH_CPU_ARM")
+    if os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "nhswe")):
+        assert bench._cpu_worker(("config4", 1, 1, 2, "adaptive"))[2] == "reference"
