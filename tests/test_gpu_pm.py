@@ -48,6 +48,19 @@ def test_rhs_and_criterion_match_reference(name):
         v = P.criterion_values(st, bathy, kind)
         r = GOLD[f"{name}_crit"][k]
         assert np.abs(v - r).max() <= 1e-12 * max(np.abs(r).max(), 1e-300), (name, kind)
+        # evaluate_criterion (nh_pm_criterion + nh_mask over m nodes): the
+        # reference's thresholded, enlarged mask of its own values, at a
+        # threshold away from every value
+        vals = np.sort(np.abs(r).max(axis=1))
+        if vals[-1] > 0.0:
+            k_nh = 0.5 * (vals[len(vals) // 2] + vals[len(vals) // 2 + 1])
+            if np.min(np.abs(np.abs(r).max(axis=1) - k_nh)) > 1e-9 * vals[-1]:
+                for enl in (False, True):
+                    want = r.max(axis=1) > k_nh
+                    if enl:
+                        want = P.enlarge_flags(want)
+                    got = P.evaluate_criterion(st, bathy, P.Criterion(kind, k_nh, enl))
+                    assert np.array_equal(got.flags, want), (name, kind, enl)
 
 
 @pytest.mark.parametrize("name", CASES)
