@@ -2,26 +2,32 @@
 //
 // One element per thread, 128-thread CTAs over tiles of OWN = 120 elements
 // plus a halo of H = 4 on each side, all CTAs independent (no clusters), so
-// the SMs run many CTAs at full occupancy and the step is bounded by HBM
-// traffic and the fp64 pipe rather than by barrier latency.  Per step:
+// the SMs run many CTAs at full occupancy.  Per step:
 //
-//   K_P  (tile)   load the tile + halo (coalesced double2 per field), finish
-//                 the previous step's correction in registers -- the
-//                 vertical-momentum update needs the solved pressure of the
-//                 neighbours, so it is fused into the NEXT step's load
-//                 ("corrector fused with the next predictor") -- then both
-//                 Heun stages (hydrostatic.py:192-209), the criterion with
-//                 +-1 enlargement (adaptivity.py:75-113), the per-element
-//                 condensation of flagged elements (corrector.py:100-349 ->
-//                 physics.cuh) and the tile's merged super-element.
-//   K_X  (member) one warp per member merges its tiles' super-elements and
-//                 hands every tile its boundary inputs (a_in, z_in).
-//   K_C  (tile)   tiles holding flagged elements only: warp/CTA merge trees
-//                 down to the elements, hu replacement and pressure p.
+//   K_P  (tile)    stream_kp.cu: load the tile + halo (coalesced double2 per
+//                  field), finish the previous step's correction in registers
+//                  -- the vertical-momentum update needs the solved pressure
+//                  of the neighbours, so it is fused into the NEXT step's load
+//                  ("corrector fused with the next predictor") -- then both
+//                  Heun stages (hydrostatic.py:192-209), the criterion with
+//                  +-1 enlargement (adaptivity.py:75-113), the flags, the
+//                  per-tile flagged count and the work list of flagged tiles.
+//   K_S  (flagged tiles, one warp per tile) LDG coefficients at t + dt
+//                  (corrector.py:100-170) stored for K_C, the per-element
+//                  condensation (corrector.py:173-349 -> physics.cuh) and the
+//                  tile's merged super-element.  Global mode: fused into K_P.
+//   K_X  (member)  one warp per member merges its tiles' super-elements and
+//                  hands every tile its boundary inputs (a_in, z_in); time,
+//                  step counter, next step's bottom-time constants, residual
+//                  gate of the previous solve.
+//   K_C  (flagged tiles) element blocks re-eliminated, warp / CTA merge trees
+//                  down to the elements, hu replacement, pressure p, residual
+//                  shares (corrector.py:355-366).
+//   K_fin (after the loop, stream_kp.cu) the last pending hw update on the
+//                  flagged tiles of the last step.
 //
-// The three launches of a step and the ping-pong of buffers are captured in
-// a CUDA graph by the host (stream.py).  A final K_P in "finalize" mode
-// applies the last pending hw update in place.
+// The launches of a step pair and the ping-pong of buffers are captured in a
+// CUDA graph by nh_stream_advance (capi.cu).
 #include "stream_kp.cuh"
 
 
