@@ -1,5 +1,5 @@
 """DRAM traffic per launch of one kernel from an `ncu --set full` report ->
-profiles/kp_traffic.json (read by bench.py for roofline.traffic).
+profiles/kp_traffic_<workload>.json (read by bench.py for roofline.traffic / fp64).
 
 usage: python tools/ncu_traffic.py rep.ncu-rep kernel_regex out.json [workload cells_per_launch]
 
