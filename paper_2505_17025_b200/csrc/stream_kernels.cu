@@ -105,7 +105,7 @@ __device__ __forceinline__ void ks_warp_tile(const StreamArgs& a, int bt, KsWarp
     }
     Super agg = S;   // tile_up's per-warp level
     if (__any_sync(0xffffffffu, flag)) {
-      agg = warp_up(agg, ws.wnode, lane, 5);
+      agg = warp_up<false>(agg, ws.wnode, lane, 5);   // K_S never sweeps down: no tree nodes
     } else {
       unsigned nonid = __ballot_sync(0xffffffffu, !is_identity(agg));
       int first = nonid ? __ffs(nonid) - 1 : 0;
@@ -116,7 +116,7 @@ __device__ __forceinline__ void ks_warp_tile(const StreamArgs& a, int bt, KsWarp
     __syncwarp();
   }
   Super v = lane < NW ? load_super(ws.wagg + lane * 6) : super_identity();
-  v = warp_up(v, ws.wnode, lane, 3);   // tile_up's cross-warp level
+  v = warp_up<false>(v, ws.wnode, lane, 3);   // tile_up's cross-warp level
   if (lane == 0) store_super(a.tile_agg + ((size_t)b * T + tile) * 8, v);
 }
 

@@ -105,7 +105,7 @@ __device__ __forceinline__ Super tile_up(Super agg, bool tflag, double* wnode, d
   const bool wany = __any_sync(0xffffffffu, tflag);
   double* wn = wnode + warp * 31 * 6;
   if (wany) {
-    agg = warp_up(agg, wn, lane, 5);
+    agg = warp_up<false>(agg, wn, lane, 5);   // aggregate only: K_C rebuilds the trees it unwinds
   } else {
     unsigned nonid = __ballot_sync(0xffffffffu, !is_identity(agg));
     int first = nonid ? __ffs(nonid) - 1 : 0;
@@ -120,7 +120,7 @@ __device__ __forceinline__ Super tile_up(Super agg, bool tflag, double* wnode, d
   Super v = super_identity();
   if (warp == 0) {
     if (lane < NW) v = load_super(wagg + lane * 6);
-    v = warp_up(v, bnode, lane, 3);
+    v = warp_up<false>(v, bnode, lane, 3);
   }
   return v;   // valid in thread 0
 }

@@ -54,6 +54,8 @@ __device__ __forceinline__ Super shfl_super(const Super& v, int src) {
 
 // Up-sweep over `levels` (count <= 2^levels lanes hold data, the rest
 // identities); lane 0 ends with the aggregate.  Node (l, k) at nodes[(base_l+k)*6].
+// STORE = false: the aggregate alone (a caller that never sweeps down, K_S).
+template <bool STORE = true>
 __device__ __forceinline__ Super warp_up(Super agg, double* nodes, int lane, int levels) {
   int base_l = 0;
   for (int l = 0; l < levels; ++l) {
@@ -62,9 +64,11 @@ __device__ __forceinline__ Super warp_up(Super agg, double* nodes, int lane, int
     if ((lane & (2 * d - 1)) == 0) {
       double AL[3], ZR[3];
       agg = merge(agg, o, AL, ZR);
-      double* nd = nodes + (base_l + (lane >> (l + 1))) * 6;
-      nd[0] = AL[0]; nd[1] = AL[1]; nd[2] = AL[2];
-      nd[3] = ZR[0]; nd[4] = ZR[1]; nd[5] = ZR[2];
+      if (STORE) {
+        double* nd = nodes + (base_l + (lane >> (l + 1))) * 6;
+        nd[0] = AL[0]; nd[1] = AL[1]; nd[2] = AL[2];
+        nd[3] = ZR[0]; nd[4] = ZR[1]; nd[5] = ZR[2];
+      }
     }
     base_l += 16 >> l;
   }
