@@ -116,7 +116,7 @@ __device__ __forceinline__ void ks_warp_tile(const StreamArgs& a, int bt, KsWarp
     __syncwarp();
   }
   Super v = lane < NW ? load_super(ws.wagg + lane * 6) : super_identity();
-  v = warp_up<false>(v, ws.wnode, lane, 3);   // tile_up's cross-warp level
+  v = warp_up<false>(v, ws.wnode, lane, NWL);   // tile_up's cross-warp level
   if (lane == 0) store_super(a.tile_agg + ((size_t)b * T + tile) * 8, v);
 }
 
@@ -375,10 +375,10 @@ __device__ __forceinline__ void kc_tile(const StreamArgs& a, int bt, KcSmem& kc)
   __syncthreads();
   if (warp == 0) {
     Super v = lane < NW ? load_super(wagg + lane * 6) : super_identity();
-    warp_up(v, bnode, lane, 3);
+    warp_up(v, bnode, lane, NWL);
     const double* io = a.tile_io + ((size_t)b * T + tile) * 2;
     double ai = lane == 0 ? io[0] : 0.0, zi = lane == 0 ? io[1] : 0.0;
-    warp_down(ai, zi, bnode, lane, 3);
+    warp_down(ai, zi, bnode, lane, NWL);
     if (lane < NW) { wio[lane * 2] = ai; wio[lane * 2 + 1] = zi; }
   }
   __syncthreads();

@@ -14,6 +14,10 @@ constexpr int TPB = NH_STREAM_THREADS;     // 128
 constexpr int H = NH_STREAM_HALO;          // 4
 constexpr int OWN = TPB - 2 * H;           // 120
 constexpr int NW = TPB / 32;
+// levels of the cross-warp tree over the NW warp aggregates (a level that
+// merges with identities only is an exact no-op, so fewer levels are bitwise
+// the same result; every caller uses this count)
+constexpr int NWL = NW <= 1 ? 0 : NW <= 2 ? 1 : NW <= 4 ? 2 : NW <= 8 ? 3 : NW <= 16 ? 4 : 5;
 
 __device__ __forceinline__ double ederiv(const nh_member& m, double v0, double v1, int i) {
   return RMUL(fma(v1, m.deriv_ref[2 * i + 1], RMUL(v0, m.deriv_ref[2 * i])), m.two_over_dx);
@@ -120,7 +124,7 @@ __device__ __forceinline__ Super tile_up(Super agg, bool tflag, double* wnode, d
   Super v = super_identity();
   if (warp == 0) {
     if (lane < NW) v = load_super(wagg + lane * 6);
-    v = warp_up<false>(v, bnode, lane, 3);
+    v = warp_up<false>(v, bnode, lane, NWL);
   }
   return v;   // valid in thread 0
 }
